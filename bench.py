@@ -1,0 +1,374 @@
+"""Benchmark driver for the B200 QuAKE hot path (one JSON line on rank 0).
+
+Headline workload: BASELINE.json configs[4], row softmax over LM vocab
+logits [4096, 128256] fp32 N(0,4), second-order QuAKE, rows sharded evenly
+across the N GPUs of the job (strong scaling; no data-path collective). A
+"step" is one pass of the hot path over the (sharded) matrix.
+
+  value  — elements/s over the whole job, inputs resident in HBM, device
+           timed with CUDA events on the launching stream, max over ranks;
+  e2e    — the same metric through the reference-facing host-span C-ABI
+           (qk_softmax_rows) from pinned host memory: H2D + kernel + D2H
+           inside the timed region;
+  roofline — algorithmic bytes (8 B/element: one read, one write) per launch
+           over the average launch duration (CUDA events), against the
+           measured HBM copy peak in MEASURED_PEAKS.json;
+  cpu_baseline — the reference's own softmax_rows (oracle/_ref, compiled in
+           place from the reference sources) on a bounded row sample, all
+           host threads, rank 0 at N=1 only.
+  per_config — rank 0 at N=1: every BASELINE config and kernel choice
+           (QuAKE, QuAKE2, expf, __expf) timed the same way, L2 flushed
+           between launches.
+
+`--impl reference` times the reference's CPU implementation instead (rank 0
+only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+BYTES_PER_ELEM = 8         # 4 B read + 4 B write, every op
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for i, nm in enumerate(names):
+                if len(s) > 5 + i and s[5 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline
+
+def cpu_reference_rate(workload, rows_per_call: int, min_seconds: float, max_calls: int,
+                       warmup: int = 1):
+    """Time the reference's own softmax_rows (or the restatement if the reference
+    was not built) on `rows_per_call` rows of the workload; returns a dict."""
+    from oracle.oracle import QUAKE, QUAKE2, best_cpu_baseline
+    impl = best_cpu_baseline()
+    cols = workload.cols
+    x = workload.host(rows_per_call * cols).reshape(rows_per_call, cols)
+    out = np.empty_like(x)
+    kern = QUAKE2 if "quake2" in workload.kernels[0] else QUAKE
+    call = (lambda: impl.softmax_rows(x, cols, workload.temperature, kern, out=out)) \
+        if impl.kind == "reference" else \
+        (lambda: impl.softmax_rows(x, cols, workload.temperature, kern))
+    for _ in range(warmup):
+        call()
+    times = []
+    t_end = time.perf_counter() + min_seconds
+    while len(times) < max_calls and (time.perf_counter() < t_end or len(times) < 3):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    n = rows_per_call * cols
+    cores = impl.effective_threads() if impl.kind == "reference" else 1
+    return {"kind": impl.kind, "cores": cores, "times": times, "elements_per_call": n,
+            "value": n * len(times) / sum(times),
+            "sample": f"{rows_per_call} rows x {cols} cols of {workload.name} "
+                      f"(QuAKE2 softmax_rows), {len(times)} calls"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2412_00408_b200.workloads import CONFIGS
+    w = CONFIGS[args.workload]
+    # each step: a bounded sample of the workload (rows) on all host threads
+    rows = args.ref_rows
+    res = cpu_reference_rate(w, rows, 0.0, args.steps, warmup=args.warmup)
+    times = res["times"]
+    value = res["value"]
+    line = {
+        "metric": "elements/s", "value": value, "unit": "elements/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": w.name, "shape": list(w.shape), "kernel": "quake2",
+                   "temperature": w.temperature, "sample_rows_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5_softmax_vocab")
+    ap.add_argument("--ref-rows", type=int, default=256)
+    ap.add_argument("--no-extras", action="store_true", help="skip per_config and cpu_baseline")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_00408_b200 as qk
+    from paper_2412_00408_b200 import _lib
+    from paper_2412_00408_b200.shard import row_shard
+    from paper_2412_00408_b200.workloads import CONFIGS
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.lib()
+    w = CONFIGS[args.workload]
+    r0, r1 = row_shard(w.rows, rank, world)
+    my_rows = r1 - r0
+    n_local = my_rows * w.cols
+    x = w.device(rows=(r0, r1)) if world > 1 else w.device()
+    y = torch.empty_like(x)
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    params = qk.SoftmaxParams(temperature=w.temperature)._c()
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    kern = int(qk.KernelChoice.Quake2)
+
+    def launch():
+        st = L.qk_softmax_rows_device(x.data_ptr(), n_local, w.cols, ctypes.byref(params), kern,
+                                      y.data_ptr(), flags.data_ptr(), sh)
+        if st != 0:
+            raise RuntimeError(_lib.last_error())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            launch()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    region0, region1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        with torch.cuda.stream(stream):
+            region0.record(stream)
+            for i in range(args.steps):
+                ev[i][0].record(stream)
+                launch()
+                ev[i][1].record(stream)
+            region1.record(stream)
+        barrier()
+    assert int(flags.item()) == 0, "non-finite flag raised on finite input"
+    region_ms = region0.elapsed_time(region1)
+    launch_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([region_ms, float(np.mean(launch_ms))], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    region_ms, kern_ms = t.tolist()
+    total_elems = w.n if world > 1 else n_local
+    value = total_elems * args.steps / (region_ms * 1e-3)
+
+    # ---- e2e through the host-span C-ABI (pinned host memory) ----
+    hx = x.cpu().pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    def host_call():
+        st = L.qk_softmax_rows(hx.data_ptr(), n_local, w.cols, ctypes.byref(params), kern,
+                               hy.data_ptr(), n_local)
+        if st != 0:
+            raise RuntimeError(_lib.last_error())
+    host_call()  # warm (workspace allocation)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        host_call()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = te.item()
+    e2e_value = total_elems * args.e2e_steps / e2e_s
+    assert torch.equal(hy.cuda(), y), "host-span path differs from the device path"
+
+    peak, peak_kind = hbm_peak()
+    achieved = BYTES_PER_ELEM * n_local / (kern_ms * 1e-3) / 1e9
+    line = {
+        "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": w.name, "shape": list(w.shape), "kernel": "quake2",
+                   "temperature": w.temperature, "rows_per_gpu": my_rows,
+                   "distribution": "N(0,4) seed 5 (torch CUDA Philox)",
+                   "l2": "inputs (2.1 GB) larger than L2 (126 MB); no flush needed",
+                   "plan": qk.softmax_plan(w.cols, True)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_kind": peak_kind, "kernel": "softmax_smem (cluster)",
+                     "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n_local,
+                     "avg_launch_us": kern_ms * 1e3},
+        "e2e": {"value": e2e_value, "unit": "elements/s",
+                "h2d_bytes_per_step": 4 * total_elems, "d2h_bytes_per_step": 4 * total_elems,
+                "path": "qk_softmax_rows (host-span C-ABI), pinned host buffers"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    traffic = _load_traffic(w.name)
+    if traffic:
+        line["roofline"]["traffic"] = traffic
+    if rank == 0 and world == 1 and not args.no_extras:
+        line["per_config"] = per_config(qk, L, _lib, peak)
+        try:
+            cb = cpu_reference_rate(w, 64, 8.0, 50)
+            line["cpu_baseline"] = {"value": cb["value"], "unit": "elements/s",
+                                    "cores": cb["cores"], "kind": cb["kind"],
+                                    "sample": cb["sample"]}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _load_traffic(workload):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+def per_config(qk, L, _lib, peak, iters=10):
+    """Every BASELINE config x kernel choice: avg kernel time with L2 flushed."""
+    import torch
+    from paper_2412_00408_b200.workloads import CFG1, CFG2, CFG3, CFG4
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # 256 MB > L2
+    res = {}
+    K = qk.KernelChoice
+
+    def timeit(fn):
+        evs = []
+        with torch.cuda.stream(stream):
+            for i in range(iters + 2):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                if i >= 2:
+                    evs.append((a, b))
+        stream.synchronize()
+        return float(np.mean([a.elapsed_time(b) for a, b in evs])) * 1e-3
+
+    for w in (CFG1, CFG2, CFG3, CFG4):
+        x = w.device()
+        y = torch.empty_like(x)
+        n = w.n
+        for kn in ("quake", "quake2", "expf", "fast_expf"):
+            k = {"quake": K.Quake, "quake2": K.Quake2, "expf": K.Expf, "fast_expf": K.FastExp}[kn]
+            if w.op == "exp":
+                fn = lambda: L.qk_exp_buffer_device(x.data_ptr(), y.data_ptr(), n, int(k), sh)
+            elif w.op == "logistic":
+                fn = lambda: L.qk_logistic_buffer_device(x.data_ptr(), y.data_ptr(), n, int(k), -1, sh)
+            elif w.op == "gelu":
+                fn = lambda: L.qk_gelu_buffer_device(x.data_ptr(), y.data_ptr(), n, int(k), -1, sh)
+            else:
+                prm = qk.SoftmaxParams(temperature=w.temperature)._c()
+                fn = lambda: L.qk_softmax_rows_device(x.data_ptr(), n, w.cols, ctypes.byref(prm),
+                                                      int(k), y.data_ptr(), None, sh)
+            s = timeit(fn)
+            gbs = BYTES_PER_ELEM * n / s / 1e9
+            res[f"{w.name}:{kn}"] = {"us": s * 1e6, "elements_per_s": n / s, "gbps": gbs,
+                                     "frac": gbs / peak}
+        del x, y
+    return res
+
+
+if __name__ == "__main__":
+    sys.exit(main())

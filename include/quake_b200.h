@@ -1,0 +1,187 @@
+/*
+ * quake_b200.h — C-ABI of the B200-native QuAKE hot path.
+ *
+ * Plain C: POD structs, raw pointers, sizes, int status codes. No C++ or
+ * torch types cross this boundary; exceptions never do. Implemented by
+ * paper_2412_00408_b200/libquake_b200.so (sm_100a kernels + C++ host layer).
+ *
+ * Each entry point replaces one public function of the reference library
+ * (paths relative to /root/reference/proj/). Three families:
+ *
+ *  1. Coefficient derivation (host-only scalar math, bit-identical to the
+ *     reference's fp64 derivations).
+ *  2. Host-span operators `qk_<op>(...)`: the drop-in for the reference's
+ *     std::span overloads. Synchronous; same preconditions, same error
+ *     categories and messages; on error `out` is left untouched (softmax
+ *     validates every row before anything is written back, nonlin.cpp:176-
+ *     180). Inputs may be pageable, pinned or device memory; work is sharded
+ *     across the devices set by qk_set_devices() (default: current device).
+ *  3. Device operators `qk_<op>_device(...)`: stream-ordered launches on
+ *     device pointers, no allocation and no synchronisation — what an
+ *     application with data already in HBM calls.
+ *
+ * KernelChoice values 0..2 match the reference enum (nonlin.hpp:32);
+ * QK_EXPF and QK_FAST_EXP are GPU-only comparison kernels of identical
+ * structure (CUDA expf / __expf in place of the QuAKE bit trick).
+ */
+#ifndef QUAKE_B200_H_
+#define QUAKE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QK_ABI_VERSION 1
+
+typedef struct CUstream_st* qk_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  QK_OK = 0,
+  /* 1..99: the reference's std::invalid_argument cases */
+  QK_ERR_SIZE_MISMATCH = 1,   /* "<op>: output size mismatch" (kernels.cpp:97-99, ...) */
+  QK_ERR_NOT_DIVISIBLE = 2,   /* "softmax_rows: length not divisible by cols" (nonlin.cpp:165-168) */
+  QK_ERR_BAD_TEMPERATURE = 3, /* "<op>: temperature must be positive" (nonlin.cpp:148-150, 172-174) */
+  QK_ERR_EMPTY_ROW = 4,       /* "softmax: empty row" (nonlin.cpp:44-46) */
+  QK_ERR_NON_FINITE = 5,      /* "softmax: non-finite input" (nonlin.cpp:49-51) */
+  QK_ERR_ZERO_SLOPE = 6,      /* "coeffs_for: input scale p must be non-zero" (kernels.cpp:27-29) */
+  QK_ERR_BAD_ARGUMENT = 7,    /* null pointer / unknown kernel choice / unsupported size */
+  /* 100+: runtime failures (no reference analogue) */
+  QK_ERR_CUDA = 100,
+  QK_ERR_NO_DEVICE = 101
+} qk_status;
+
+typedef enum {
+  QK_EXACT = 0,   /* reference KernelChoice::Exact (libm-style expf / tanhf) */
+  QK_QUAKE = 1,   /* KernelChoice::Quake  — first-order bit-trick exp */
+  QK_QUAKE2 = 2,  /* KernelChoice::Quake2 — second-order mantissa refinement */
+  QK_EXPF = 3,    /* comparison: QuAKE structure with CUDA expf */
+  QK_FAST_EXP = 4 /* comparison: QuAKE structure with __expf */
+} qk_kernel;
+
+/* kernels.hpp:39-46 AffineCoeffs */
+typedef struct {
+  float c0;
+  float c1;
+  float input_scale; /* p */
+  float input_shift; /* q */
+  int32_t bias_applied;
+} qk_affine_coeffs;
+
+/* kernels.hpp:60-76 QuadCoeffs */
+typedef struct {
+  float a0, a1, a2;
+} qk_quad_coeffs;
+
+/* kernels.hpp:81-84 ClampRange */
+typedef struct {
+  float lo, hi;
+} qk_clamp_range;
+
+/* nonlin.hpp:43-49 SoftmaxParams; centering_bias: -1 = unset (per-kernel
+ * default, nonlin.hpp:39-41), 0 = off, 1 = on. */
+typedef struct {
+  float temperature;
+  int32_t centering_bias;
+  qk_quad_coeffs quad;
+} qk_softmax_params;
+
+/* nonlin.hpp:55-62 GeluConstants */
+typedef struct {
+  float kappa, root2_over_pi, fused_scale, inverse_kappa;
+} qk_gelu_constants;
+
+/* Softmax launch plan (introspection; the reduction geometry that fixes the
+ * summation order, see softmax.cu). */
+typedef struct {
+  int32_t variant; /* 0 warp/float4, 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep */
+  int32_t width;   /* elements per chunk: 4 or 1 */
+  int32_t lanes;   /* partial-sum lanes per CTA */
+  int32_t cluster; /* CTAs per row */
+  int64_t slice;   /* chunks per CTA slice (0 = whole row) */
+  int32_t threads; /* CTA size */
+  int32_t vpt;     /* warp variants: chunks per lane */
+  int64_t smem;    /* dynamic smem bytes per CTA */
+} qk_softmax_plan_info;
+
+/* ---- library ---- */
+int qk_abi_version(void);
+const char* qk_last_error(void);        /* message of the last failure on this thread */
+int qk_is_invalid_argument(qk_status s);/* 1 for the std::invalid_argument family */
+qk_status qk_device_count(int* count);
+/* Devices the host-span operators shard over (rows / 16-byte element
+ * ranges, no collectives). n = 0 restores the default (current device). */
+qk_status qk_set_devices(const int* devices, int n);
+int qk_get_devices(int* devices, int cap);
+/* Frees cached device workspace and pinned staging used by the host-span path. */
+void qk_release_workspace(void);
+
+/* ---- 1. coefficient derivation (kernels.cpp:25-87, nonlin.cpp:132-141) ---- */
+qk_status qk_coeffs_for(float p, float q, int32_t centering_bias, qk_affine_coeffs* out);
+qk_affine_coeffs qk_natural_exp_coeffs(int32_t centering_bias);
+qk_affine_coeffs qk_base2_coeffs(int32_t centering_bias);
+qk_affine_coeffs qk_negated_natural_exp_coeffs(int32_t centering_bias);
+qk_status qk_default_clamp(float p, float q, qk_clamp_range* out);
+qk_clamp_range qk_clamp_for(const qk_affine_coeffs* c);
+qk_quad_coeffs qk_quad_continuity(void);
+qk_quad_coeffs qk_quad_minimax(void);
+int qk_quad_is_continuity_default(const qk_quad_coeffs* a);
+qk_gelu_constants qk_gelu_constants_defaults(void);
+int32_t qk_resolve_centering_bias(qk_kernel k, int32_t requested);
+const char* qk_kernel_name(qk_kernel k);
+qk_status qk_softmax_plan(size_t cols, int32_t aligned16, qk_softmax_plan_info* out);
+
+/* ---- 2. host-span operators (drop-ins for the std::span overloads) ---- */
+/* kernels.hpp:163-164 / kernels.cpp:95-107 quake_buffer */
+qk_status qk_quake_buffer(const float* xs, size_t n, float* out, size_t out_n,
+                          const qk_affine_coeffs* c, const qk_clamp_range* r);
+/* kernels.hpp:165-167 / kernels.cpp:109-136 quake2_buffer */
+qk_status qk_quake2_buffer(const float* xs, size_t n, float* out, size_t out_n,
+                           const qk_affine_coeffs* c, const qk_quad_coeffs* a,
+                           const qk_clamp_range* r);
+/* nonlin.hpp:86-88 / nonlin.cpp:210-243 logistic_buffer */
+qk_status qk_logistic_buffer(const float* xs, size_t n, float* out, size_t out_n, qk_kernel k,
+                             int32_t centering_bias);
+/* nonlin.hpp:95-97 / nonlin.cpp:292-330 gelu_buffer */
+qk_status qk_gelu_buffer(const float* xs, size_t n, float* out, size_t out_n, qk_kernel k,
+                         int32_t centering_bias);
+/* nonlin.hpp:77-79 / nonlin.cpp:162-189 softmax_rows */
+qk_status qk_softmax_rows(const float* matrix, size_t n, size_t cols,
+                          const qk_softmax_params* params, qk_kernel k, float* out,
+                          size_t out_n);
+/* nonlin.hpp:70-71 / nonlin.cpp:143-153 softmax_row */
+qk_status qk_softmax_row(const float* v, size_t n, const qk_softmax_params* params, qk_kernel k,
+                         float* out, size_t out_n);
+/* exp comparison (bench.cpp:236-258 make_exp_pass analogue): QK_EXACT/QK_EXPF
+ * = expf, QK_FAST_EXP = __expf, QK_QUAKE/QK_QUAKE2 = natural-exp QuAKE with
+ * the per-kernel default bias. */
+qk_status qk_exp_buffer(const float* xs, size_t n, float* out, size_t out_n, qk_kernel k);
+
+/* ---- 3. device operators (stream-ordered, device pointers, no sync) ---- */
+qk_status qk_quake_buffer_device(const float* xs, float* out, size_t n,
+                                 const qk_affine_coeffs* c, const qk_clamp_range* r,
+                                 qk_stream stream);
+qk_status qk_quake2_buffer_device(const float* xs, float* out, size_t n,
+                                  const qk_affine_coeffs* c, const qk_quad_coeffs* a,
+                                  const qk_clamp_range* r, qk_stream stream);
+qk_status qk_logistic_buffer_device(const float* xs, float* out, size_t n, qk_kernel k,
+                                    int32_t centering_bias, qk_stream stream);
+qk_status qk_gelu_buffer_device(const float* xs, float* out, size_t n, qk_kernel k,
+                                int32_t centering_bias, qk_stream stream);
+qk_status qk_exp_buffer_device(const float* xs, float* out, size_t n, qk_kernel k,
+                               qk_stream stream);
+/* Row softmax on device memory. Shape/temperature are validated on the host
+ * before launch; non-finite inputs are detected inside the kernel's max pass
+ * and reported by OR-ing 1 into *d_flags (device word, may be NULL). Unlike
+ * the host-span form, `out` may already be written when that happens. */
+qk_status qk_softmax_rows_device(const float* matrix, size_t n, size_t cols,
+                                 const qk_softmax_params* params, qk_kernel k, float* out,
+                                 uint32_t* d_flags, qk_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QUAKE_B200_H_ */

@@ -1,0 +1,188 @@
+// TEST INFRASTRUCTURE ONLY — extern "C" wrappers around the reference
+// library, compiled in place from /root/reference/proj/core/src by
+// oracle/Makefile into oracle/_ref/libquake_ref.so. Used by tests/ (to pin
+// the C restatement and to generate tests/golden/), and by bench.py's
+// cpu_baseline and --impl reference legs (the reference's own CPU path,
+// timed on the host cores). Never linked into the product library.
+//
+// Each wrapper calls exactly one public reference entry point:
+//   kernels.hpp:163-171 quake_buffer / quake2_buffer
+//   nonlin.hpp:70-97    softmax_row(s), logistic_buffer, gelu_buffer
+//   kernels.hpp:47-51, 86-88   coeffs_for / clamp_for / default_clamp
+//   oracle.hpp:28-42    exact_* ground truth
+#include <cstring>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+
+#include "quake/kernels.hpp"
+#include "quake/nonlin.hpp"
+#include "quake/oracle.hpp"
+#include "quake/parallel.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+quake::KernelChoice kernel_of(int k) {
+  switch (k) {
+    case 1: return quake::KernelChoice::Quake;
+    case 2: return quake::KernelChoice::Quake2;
+    default: return quake::KernelChoice::Exact;
+  }
+}
+
+std::optional<bool> bias_of(int b) {
+  if (b < 0) return std::nullopt;
+  return b != 0;
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 2;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_last_error.c_str(); }
+
+unsigned ref_effective_threads() { return quake::effective_threads(); }
+
+int ref_coeffs_for(float p, float q, int bias, float* c0, float* c1) {
+  return guarded([&] {
+    const quake::AffineCoeffs c = quake::coeffs_for(p, q, quake::kSingle, bias != 0);
+    *c0 = c.c0;
+    *c1 = c.c1;
+  });
+}
+
+int ref_default_clamp(float p, float q, float* lo, float* hi) {
+  return guarded([&] {
+    const quake::ClampRange r = quake::default_clamp(p, q);
+    *lo = r.lo;
+    *hi = r.hi;
+  });
+}
+
+void ref_clamp_for(float c0, float c1, float* lo, float* hi) {
+  quake::AffineCoeffs c{c0, c1, 0.0f, 0.0f, false};
+  const quake::ClampRange r = quake::clamp_for(c);
+  *lo = r.lo;
+  *hi = r.hi;
+}
+
+void ref_named_coeffs(int which, int bias, float* c0, float* c1) {
+  // 0 natural, 1 base2, 2 negated natural (kernels.cpp:42-54)
+  quake::AffineCoeffs c = which == 0   ? quake::natural_exp_coeffs(bias != 0)
+                          : which == 1 ? quake::base2_coeffs(bias != 0)
+                                       : quake::negated_natural_exp_coeffs(bias != 0);
+  *c0 = c.c0;
+  *c1 = c.c1;
+}
+
+float ref_quake(float x, float c0, float c1, float lo, float hi) {
+  quake::AffineCoeffs c{c0, c1, 0.0f, 0.0f, false};
+  return quake::quake(x, c, quake::ClampRange{lo, hi});
+}
+
+float ref_quake2(float x, float c0, float c1, float a0, float a1, float a2, float lo,
+                 float hi) {
+  quake::AffineCoeffs c{c0, c1, 0.0f, 0.0f, false};
+  return quake::quake2(x, c, quake::QuadCoeffs{a0, a1, a2}, quake::ClampRange{lo, hi});
+}
+
+int ref_quake_buffer(const float* xs, size_t n, float* out, float c0, float c1, float lo,
+                     float hi) {
+  return guarded([&] {
+    quake::AffineCoeffs c{c0, c1, 0.0f, 0.0f, false};
+    quake::quake_buffer(std::span<const float>(xs, n), std::span<float>(out, n), c,
+                        quake::ClampRange{lo, hi});
+  });
+}
+
+int ref_quake2_buffer(const float* xs, size_t n, float* out, float c0, float c1, float a0,
+                      float a1, float a2, float lo, float hi) {
+  return guarded([&] {
+    quake::AffineCoeffs c{c0, c1, 0.0f, 0.0f, false};
+    quake::quake2_buffer(std::span<const float>(xs, n), std::span<float>(out, n), c,
+                         quake::QuadCoeffs{a0, a1, a2}, quake::ClampRange{lo, hi});
+  });
+}
+
+int ref_logistic_buffer(const float* xs, size_t n, float* out, int kernel, int bias) {
+  return guarded([&] {
+    quake::logistic_buffer(std::span<const float>(xs, n), std::span<float>(out, n),
+                           kernel_of(kernel), bias_of(bias));
+  });
+}
+
+int ref_gelu_buffer(const float* xs, size_t n, float* out, int kernel, int bias) {
+  return guarded([&] {
+    quake::gelu_buffer(std::span<const float>(xs, n), std::span<float>(out, n),
+                       kernel_of(kernel), bias_of(bias));
+  });
+}
+
+float ref_logistic(float x, int kernel, int bias) {
+  return quake::logistic(x, kernel_of(kernel), bias_of(bias));
+}
+
+float ref_gelu(float x, int kernel, int bias) {
+  return quake::gelu(x, kernel_of(kernel), bias_of(bias));
+}
+
+int ref_softmax_rows(const float* m, size_t n, size_t cols, float temperature, int bias,
+                     float a0, float a1, float a2, int kernel, float* out, size_t out_n) {
+  return guarded([&] {
+    quake::SoftmaxParams p;
+    p.temperature = temperature;
+    p.centering_bias = bias_of(bias);
+    p.quad = quake::QuadCoeffs{a0, a1, a2};
+    quake::softmax_rows(std::span<const float>(m, n), cols, p, kernel_of(kernel),
+                        std::span<float>(out, out_n));
+  });
+}
+
+int ref_softmax_row(const float* v, size_t n, float temperature, int bias, float a0,
+                    float a1, float a2, int kernel, float* out, size_t out_n) {
+  return guarded([&] {
+    quake::SoftmaxParams p;
+    p.temperature = temperature;
+    p.centering_bias = bias_of(bias);
+    p.quad = quake::QuadCoeffs{a0, a1, a2};
+    quake::softmax_row(std::span<const float>(v, n), p, kernel_of(kernel),
+                       std::span<float>(out, out_n));
+  });
+}
+
+void ref_gelu_constants(float* kappa, float* r2pi, float* fused_scale, float* inverse_kappa) {
+  const quake::GeluConstants g = quake::GeluConstants::defaults();
+  *kappa = g.kappa;
+  *r2pi = g.root2_over_pi;
+  *fused_scale = g.fused_scale;
+  *inverse_kappa = g.inverse_kappa;
+}
+
+double ref_exact_exp(double x) { return quake::oracle::exact_exp(x); }
+double ref_exact_logistic(double x) { return quake::oracle::exact_logistic(x); }
+double ref_exact_gelu_tanh(double x) { return quake::oracle::exact_gelu_tanh(x); }
+
+int ref_exact_softmax(const float* v, size_t n, double t, double* out) {
+  return guarded([&] {
+    quake::oracle::exact_softmax(std::span<const float>(v, n), t, std::span<double>(out, n));
+  });
+}
+
+}  // extern "C"

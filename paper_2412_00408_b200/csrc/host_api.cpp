@@ -1,0 +1,806 @@
+// C++ host layer of libquake_b200.so: implements include/quake_b200.h.
+//
+//  * coefficient derivation — bit-identical restatement of the reference's
+//    fp64 derivations (kernels.cpp:25-87, nonlin.cpp:35-41, 85-93, 132-141,
+//    248-264); compiled with -ffp-contract=off like the reference build;
+//  * validation with the reference's preconditions, order and messages;
+//  * dispatch to the sm_100a kernels (elementwise.cu, softmax.cu);
+//  * the host-span path: per-device cached workspace, chunked H2D / kernel /
+//    D2H pipelines over three streams, and the multi-GPU driver that shards
+//    rows (softmax) or 16-byte-aligned element ranges (elementwise) over the
+//    configured devices with one host thread per device and no collectives
+//    — the GPU replacement of parallel_chunks (parallel.hpp:43-68).
+// Reference paths cited relative to /root/reference/proj/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <barrier>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/quake_b200.h"
+#include "internal.h"
+
+namespace {
+
+// std::numbers::log2e / ln2 / pi as exact binary64 values.
+constexpr double kLog2e = 0x1.71547652b82fep+0;
+constexpr double kLn2 = 0x1.62e42fefa39efp-1;
+constexpr double kPi = 0x1.921fb54442d18p+1;
+constexpr double kCenteringBias = 0.0436;  // kernels.hpp:29
+constexpr double kScale = 8388608.0;       // 2^23 = ldexp(1, mantissa_bits)
+constexpr double kLowExponentEdge = 1.01;  // kernels.cpp:63
+constexpr double kHighExponentEdge = 254.99;  // kernels.cpp:64
+
+thread_local std::string g_error;
+
+qk_status fail(qk_status s, const std::string& msg) {
+  g_error = msg;
+  return s;
+}
+
+qk_status cuda_fail(cudaError_t e, const char* where) {
+  g_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return QK_ERR_CUDA;
+}
+
+#define QK_CUDA(call, where)                          \
+  do {                                                \
+    cudaError_t qk_e_ = (call);                       \
+    if (qk_e_ != cudaSuccess) return cuda_fail(qk_e_, where); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// coefficient derivation
+
+qk_affine_coeffs make_coeffs(float p, float q, bool bias) {
+  // kernels.cpp:30-39
+  const double beta = bias ? kCenteringBias : 0.0;
+  qk_affine_coeffs c;
+  c.c0 = static_cast<float>(kScale * static_cast<double>(p));
+  c.c1 = static_cast<float>(kScale * (static_cast<double>(127) + static_cast<double>(q) - beta));
+  c.input_scale = p;
+  c.input_shift = q;
+  c.bias_applied = bias ? 1 : 0;
+  return c;
+}
+
+qk_clamp_range solve_clamp(double c0, double c1) {
+  // kernels.cpp:64-70
+  double a = (kLowExponentEdge * kScale - c1) / c0;
+  double b = (kHighExponentEdge * kScale - c1) / c0;
+  if (a > b) std::swap(a, b);
+  return {static_cast<float>(a), static_cast<float>(b)};
+}
+
+bool is_continuity(const qk_quad_coeffs& a) {
+  // kernels.hpp:73-75
+  return a.a0 == 1.0f / 3.0f && a.a1 == 0.0f && a.a2 == 2.0f / 3.0f;
+}
+
+bool resolve_bias(qk_kernel k, int32_t requested) {
+  // nonlin.hpp:39-41
+  return requested < 0 ? (k == QK_QUAKE) : (requested != 0);
+}
+
+qk_gelu_constants gelu_defaults() {
+  // nonlin.cpp:132-141
+  constexpr double kappa = 0.044715;
+  const double root2_over_pi = std::sqrt(2.0 / kPi);
+  qk_gelu_constants g;
+  g.kappa = static_cast<float>(kappa);
+  g.root2_over_pi = static_cast<float>(root2_over_pi);
+  g.fused_scale = static_cast<float>(2.0 * kappa * root2_over_pi);
+  g.inverse_kappa = static_cast<float>(1.0 / kappa);
+  return g;
+}
+
+// fl(fl(c0*x) + c1) inside int32 range?
+bool z_in_range(float c0, float x, float c1) {
+  volatile float prod = c0 * x;
+  volatile float z = prod + c1;
+  return z >= -2147483648.0f && z < 2147483648.0f;
+}
+
+// Does saturate(x) in [lo, hi] keep c0*x+c1 inside int32 for every x
+// (including NaN -> hi)? If not, the kernel emulates x86 cvttss2si.
+bool needs_x86_overflow(const qk_affine_coeffs& c, const qk_clamp_range& r) {
+  if (!std::isfinite(c.c0) || !std::isfinite(c.c1) || std::isnan(r.lo) || std::isnan(r.hi)) {
+    return true;
+  }
+  return !(z_in_range(c.c0, r.lo, c.c1) && z_in_range(c.c0, r.hi, c.c1));
+}
+
+// ---------------------------------------------------------------------------
+// devices
+
+std::mutex g_dev_mu;
+std::vector<int> g_devices;  // empty = current device
+
+std::vector<int> active_devices() {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_devices.empty()) return g_devices;
+  int d = 0;
+  cudaGetDevice(&d);
+  return {d};
+}
+
+struct DeviceState {
+  std::mutex mu;  // serialises host-span calls on this device
+  int sm_count = 0;
+  float* d_in = nullptr;
+  float* d_out = nullptr;
+  size_t cap = 0;  // floats
+  uint32_t* d_flags = nullptr;
+  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+};
+
+constexpr int kMaxDevices = 64;
+DeviceState g_state[kMaxDevices];
+std::mutex g_sm_mu;
+
+int sm_count_of(int dev) {
+  DeviceState& st = g_state[dev];
+  if (st.sm_count == 0) {
+    std::lock_guard<std::mutex> lk(g_sm_mu);
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+      v = 148;
+    }
+    st.sm_count = v;
+  }
+  return st.sm_count;
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// Caller holds st.mu and has set the device.
+qk_status ensure_workspace(DeviceState& st, size_t n) {
+  if (st.streams[0] == nullptr) {
+    for (auto& s : st.streams) QK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    QK_CUDA(cudaMalloc(&st.d_flags, sizeof(uint32_t)), "cudaMalloc(flags)");
+  }
+  if (n > st.cap) {
+    if (st.d_in) cudaFree(st.d_in);
+    if (st.d_out) cudaFree(st.d_out);
+    st.d_in = st.d_out = nullptr;
+    st.cap = 0;
+    const size_t want = std::max<size_t>(n, 1 << 20);
+    QK_CUDA(cudaMalloc(&st.d_in, want * sizeof(float)), "cudaMalloc(workspace in)");
+    QK_CUDA(cudaMalloc(&st.d_out, want * sizeof(float)), "cudaMalloc(workspace out)");
+    st.cap = want;
+  }
+  return QK_OK;
+}
+
+bool device_pointer(const void* p, int* dev) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    *dev = a.device;
+    return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// elementwise resolution
+
+enum class Family { kQuake, kQuake2, kLogistic, kGelu, kExp };
+
+struct EwSpec {
+  qk::EwOp op;
+  qk::EwParams p;
+};
+
+qk_status resolve_ew(Family f, qk_kernel k, int32_t bias_req, const qk_affine_coeffs* c,
+                     const qk_clamp_range* r, const qk_quad_coeffs* a, EwSpec* out) {
+  qk::EwParams p{};
+  switch (f) {
+    case Family::kQuake:
+    case Family::kQuake2: {
+      p.c0 = c->c0;
+      p.c1 = c->c1;
+      p.lo = r->lo;
+      p.hi = r->hi;
+      p.x86_overflow = needs_x86_overflow(*c, *r) ? 1 : 0;
+      if (f == Family::kQuake) {
+        out->op = qk::EwOp::kQuake;
+      } else if (is_continuity(*a)) {
+        out->op = qk::EwOp::kQuake2;
+      } else {
+        out->op = qk::EwOp::kQuake2General;
+        p.a0 = a->a0;
+        p.a1 = a->a1;
+        p.a2 = a->a2;
+      }
+      break;
+    }
+    case Family::kExp: {
+      if (k == QK_EXACT || k == QK_EXPF) {
+        out->op = qk::EwOp::kExpExpf;
+      } else if (k == QK_FAST_EXP) {
+        out->op = qk::EwOp::kExpFast;
+      } else if (k == QK_QUAKE || k == QK_QUAKE2) {
+        // quake_cli.cpp:277-289: natural-exp coefficients, per-kernel bias.
+        const qk_affine_coeffs ce = make_coeffs(static_cast<float>(kLog2e), 0.0f,
+                                                resolve_bias(k, bias_req));
+        const qk_clamp_range rc = solve_clamp(ce.c0, ce.c1);
+        p.c0 = ce.c0;
+        p.c1 = ce.c1;
+        p.lo = rc.lo;
+        p.hi = rc.hi;
+        out->op = k == QK_QUAKE ? qk::EwOp::kQuake : qk::EwOp::kQuake2;
+      } else {
+        return fail(QK_ERR_BAD_ARGUMENT, "exp_buffer: unknown kernel choice");
+      }
+      break;
+    }
+    case Family::kLogistic: {
+      if (k == QK_EXACT || k == QK_EXPF) {
+        out->op = qk::EwOp::kLogisticExpf;
+      } else if (k == QK_FAST_EXP) {
+        out->op = qk::EwOp::kLogisticFast;
+      } else if (k == QK_QUAKE || k == QK_QUAKE2) {
+        // nonlin.cpp:35-41 negated_exp_kernel
+        const qk_affine_coeffs ce = make_coeffs(static_cast<float>(-kLog2e), 0.0f,
+                                                resolve_bias(k, bias_req));
+        const qk_clamp_range rc = solve_clamp(ce.c0, ce.c1);
+        p.c0 = ce.c0;
+        p.c1 = ce.c1;
+        p.lo = rc.lo;
+        p.hi = rc.hi;
+        out->op = k == QK_QUAKE ? qk::EwOp::kLogisticQuake : qk::EwOp::kLogisticQuake2;
+      } else {
+        return fail(QK_ERR_BAD_ARGUMENT, "logistic_buffer: unknown kernel choice");
+      }
+      break;
+    }
+    case Family::kGelu: {
+      const qk_gelu_constants g = gelu_defaults();
+      p.k0 = g.inverse_kappa;
+      p.k1 = g.kappa;
+      p.k2 = g.root2_over_pi;
+      if (k == QK_EXACT) {
+        out->op = qk::EwOp::kGeluTanh;
+      } else if (k == QK_EXPF || k == QK_FAST_EXP) {
+        p.c0 = -g.fused_scale;
+        out->op = k == QK_EXPF ? qk::EwOp::kGeluExpf : qk::EwOp::kGeluFast;
+      } else if (k == QK_QUAKE || k == QK_QUAKE2) {
+        // nonlin.cpp:248-264 gelu_exp_kernel
+        const qk_affine_coeffs ce =
+            make_coeffs(static_cast<float>(-kLog2e * static_cast<double>(g.fused_scale)), 0.0f,
+                        resolve_bias(k, bias_req));
+        const qk_clamp_range rc = solve_clamp(ce.c0, ce.c1);
+        p.c0 = ce.c0;
+        p.c1 = ce.c1;
+        p.lo = rc.lo;
+        p.hi = rc.hi;
+        out->op = k == QK_QUAKE ? qk::EwOp::kGeluQuake : qk::EwOp::kGeluQuake2;
+      } else {
+        return fail(QK_ERR_BAD_ARGUMENT, "gelu_buffer: unknown kernel choice");
+      }
+      break;
+    }
+  }
+  out->p = p;
+  return QK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// softmax resolution (nonlin.cpp:71-116)
+
+qk_status resolve_sm(const qk_softmax_params* prm, qk_kernel k, qk::SmKernel* sk,
+                     qk::SmParams* sp) {
+  const float t = prm->temperature;
+  qk::SmParams p{};
+  p.t = t;
+  const double beta = resolve_bias(k, prm->centering_bias) ? kCenteringBias : 0.0;
+  p.c0 = static_cast<float>(kScale * static_cast<double>(t) * kLog2e);  // nonlin.cpp:89
+  p.c1_base = kScale * (static_cast<double>(127) - beta);               // nonlin.cpp:90-91
+  p.vmin_off = 126.0 * kLn2 / static_cast<double>(t);                   // nonlin.cpp:92-93
+  switch (k) {
+    case QK_EXACT: *sk = qk::SmKernel::kExact; break;
+    case QK_EXPF: *sk = qk::SmKernel::kExpf; break;
+    case QK_FAST_EXP: *sk = qk::SmKernel::kFast; break;
+    case QK_QUAKE: *sk = qk::SmKernel::kQuake; break;
+    case QK_QUAKE2:
+      if (is_continuity(prm->quad)) {
+        *sk = qk::SmKernel::kQuake2;
+      } else {
+        *sk = qk::SmKernel::kQuake2General;
+        p.a0 = prm->quad.a0;
+        p.a1 = prm->quad.a1;
+        p.a2 = prm->quad.a2;
+      }
+      break;
+    default: return fail(QK_ERR_BAD_ARGUMENT, "softmax: unknown kernel choice");
+  }
+  *sp = p;
+  return QK_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+// host-span drivers
+
+// Run fn(device, begin, end) for each device's shard, one host thread per
+// device beyond the first; returns the first failing status.
+template <typename Fn>
+qk_status for_each_shard(const std::vector<std::pair<size_t, size_t>>& shards,
+                         const std::vector<int>& devs, Fn&& fn) {
+  const size_t nd = devs.size();
+  std::vector<qk_status> st(nd, QK_OK);
+  std::vector<std::string> err(nd);
+  auto run = [&](size_t i) {
+    // fn always runs (dev = -1 when the device cannot be selected) so that
+    // shard functions which rendezvous with their siblings never deadlock.
+    const int dev = cudaSetDevice(devs[i]) == cudaSuccess ? devs[i] : -1;
+    st[i] = fn(i, dev, shards[i].first, shards[i].second);
+    err[i] = g_error;
+  };
+  int prev = current_device();
+  std::vector<std::thread> pool;
+  for (size_t i = 1; i < nd; ++i) pool.emplace_back(run, i);
+  run(0);
+  for (auto& t : pool) t.join();
+  cudaSetDevice(prev);
+  for (size_t i = 0; i < nd; ++i) {
+    if (st[i] != QK_OK) {
+      g_error = err[i];
+      return st[i];
+    }
+  }
+  return QK_OK;
+}
+
+// Contiguous shards of n units; boundaries multiples of `align` units.
+std::vector<std::pair<size_t, size_t>> make_shards(size_t n, size_t parts, size_t align) {
+  std::vector<std::pair<size_t, size_t>> s(parts);
+  const size_t units = (n + align - 1) / align;
+  size_t begin = 0;
+  for (size_t i = 0; i < parts; ++i) {
+    const size_t u = units / parts + (i < units % parts ? 1 : 0);
+    const size_t end = std::min(n, begin + u * align);
+    s[i] = {begin, end};
+    begin = end;
+  }
+  return s;
+}
+
+constexpr size_t kChunkElems = size_t{16} << 20;  // 64 MiB per pipeline stage
+
+qk_status run_elementwise_host(const EwSpec& spec, const float* xs, float* out, size_t n) {
+  if (n == 0) return QK_OK;
+  int pdev = 0;
+  const bool in_dev = device_pointer(xs, &pdev);
+  int odev = 0;
+  const bool out_dev = device_pointer(out, &odev);
+  if (in_dev && out_dev) {
+    // Device spans: one launch on the owning device, synchronous.
+    int prev = current_device();
+    cudaSetDevice(pdev);
+    cudaError_t e = qk::launch_elementwise(spec.op, xs, out, n, spec.p, sm_count_of(pdev), nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "elementwise kernel");
+    return QK_OK;
+  }
+  std::vector<int> devs = in_dev ? std::vector<int>{pdev} : (out_dev ? std::vector<int>{odev}
+                                                                      : active_devices());
+  const auto shards = make_shards(n, devs.size(), 4);
+  return for_each_shard(shards, devs, [&](size_t, int dev, size_t b, size_t e) -> qk_status {
+    const size_t len = e - b;
+    if (dev < 0) return fail(QK_ERR_NO_DEVICE, "cudaSetDevice failed");
+    if (len == 0) return QK_OK;
+    DeviceState& st = g_state[dev];
+    std::lock_guard<std::mutex> lk(st.mu);
+    qk_status s = ensure_workspace(st, len);
+    if (s != QK_OK) return s;
+    const int sms = sm_count_of(dev);
+    size_t ci = 0;
+    for (size_t off = 0; off < len; off += kChunkElems, ++ci) {
+      const size_t cl = std::min(kChunkElems, len - off);
+      cudaStream_t str = st.streams[ci % 3];
+      const float* src = xs + b + off;
+      float* dsrc = st.d_in + off;
+      if (in_dev) {
+        dsrc = const_cast<float*>(src);
+      } else {
+        QK_CUDA(cudaMemcpyAsync(dsrc, src, cl * sizeof(float), cudaMemcpyHostToDevice, str), "H2D");
+      }
+      float* ddst = out_dev ? out + b + off : st.d_out + off;
+      QK_CUDA(qk::launch_elementwise(spec.op, dsrc, ddst, cl, spec.p, sms, str), "elementwise kernel");
+      if (!out_dev) {
+        QK_CUDA(cudaMemcpyAsync(out + b + off, ddst, cl * sizeof(float), cudaMemcpyDeviceToHost, str),
+                "D2H");
+      }
+    }
+    for (auto& str : st.streams) QK_CUDA(cudaStreamSynchronize(str), "stream sync");
+    return QK_OK;
+  });
+}
+
+qk_status validate_sm(const char* who, size_t n, size_t cols, const qk_softmax_params* prm,
+                      size_t out_n, bool single_row) {
+  if (single_row) {
+    // nonlin.cpp:145-153
+    if (out_n != n) return fail(QK_ERR_SIZE_MISMATCH, std::string(who) + ": output size mismatch");
+    if (!(prm->temperature > 0.0f)) {
+      return fail(QK_ERR_BAD_TEMPERATURE, std::string(who) + ": temperature must be positive");
+    }
+    if (n == 0) return fail(QK_ERR_EMPTY_ROW, "softmax: empty row");
+    return QK_OK;
+  }
+  // nonlin.cpp:165-175
+  if (cols == 0 || n % cols != 0) {
+    return fail(QK_ERR_NOT_DIVISIBLE, std::string(who) + ": length not divisible by cols");
+  }
+  if (out_n != n) return fail(QK_ERR_SIZE_MISMATCH, std::string(who) + ": output size mismatch");
+  if (!(prm->temperature > 0.0f)) {
+    return fail(QK_ERR_BAD_TEMPERATURE, std::string(who) + ": temperature must be positive");
+  }
+  return QK_OK;
+}
+
+qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softmax_params* prm,
+                           qk_kernel k, float* out) {
+  qk::SmKernel sk;
+  qk::SmParams sp;
+  qk_status s = resolve_sm(prm, k, &sk, &sp);
+  if (s != QK_OK) return s;
+  const size_t rows = n / cols;
+  if (rows == 0) return QK_OK;
+  int pdev = 0, odev = 0;
+  const bool in_dev = device_pointer(m, &pdev);
+  const bool out_dev = device_pointer(out, &odev);
+  std::vector<int> devs = in_dev ? std::vector<int>{pdev} : (out_dev ? std::vector<int>{odev}
+                                                                      : active_devices());
+  const auto shards = make_shards(rows, devs.size(), 1);
+  std::atomic<bool> non_finite{false};
+  std::atomic<bool> abort_all{false};
+  std::barrier sync_point(static_cast<std::ptrdiff_t>(devs.size()));
+  const size_t chunk_rows = std::max<size_t>(1, kChunkElems / cols);
+
+  s = for_each_shard(shards, devs, [&](size_t, int dev, size_t rb, size_t re) -> qk_status {
+    if (dev < 0) {
+      abort_all.store(true);
+      sync_point.arrive_and_wait();
+      return fail(QK_ERR_NO_DEVICE, "cudaSetDevice failed");
+    }
+    DeviceState& st = g_state[dev];
+    std::unique_lock<std::mutex> lk(st.mu);
+    const size_t nrows = re - rb;
+    qk_status ss = ensure_workspace(st, nrows * cols);
+    const float* dsrc_all = in_dev ? m + rb * cols : st.d_in;
+    float* ddst_all = out_dev ? out + rb * cols : st.d_out;
+    const qk::SmPlan plan = qk::plan_softmax(cols, aligned16(dsrc_all) && aligned16(ddst_all), dev);
+    if (ss == QK_OK && cudaMemsetAsync(st.d_flags, 0, sizeof(uint32_t), st.streams[0]) != cudaSuccess) {
+      ss = fail(QK_ERR_CUDA, "cudaMemset(flags)");
+    }
+    if (ss == QK_OK) cudaStreamSynchronize(st.streams[0]);
+    // Phase 1: H2D + kernels (every row validated in the max pass).
+    size_t ci = 0;
+    for (size_t r0 = 0; ss == QK_OK && r0 < nrows; r0 += chunk_rows, ++ci) {
+      const size_t cr = std::min(chunk_rows, nrows - r0);
+      cudaStream_t str = st.streams[ci % 3];
+      const float* dsrc = dsrc_all + r0 * cols;
+      if (!in_dev) {
+        if (cudaMemcpyAsync(st.d_in + r0 * cols, m + (rb + r0) * cols, cr * cols * sizeof(float),
+                            cudaMemcpyHostToDevice, str) != cudaSuccess) {
+          ss = fail(QK_ERR_CUDA, "H2D");
+          break;
+        }
+      }
+      cudaError_t e = qk::launch_softmax(sk, plan, dsrc, ddst_all + r0 * cols, cr, cols, sp,
+                                         st.d_flags, str);
+      if (e != cudaSuccess) ss = cuda_fail(e, "softmax kernel");
+    }
+    uint32_t flags = 0;
+    for (auto& str : st.streams) {
+      if (cudaStreamSynchronize(str) != cudaSuccess && ss == QK_OK) ss = fail(QK_ERR_CUDA, "stream sync");
+    }
+    if (ss == QK_OK && cudaMemcpy(&flags, st.d_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
+                           cudaSuccess) {
+      ss = fail(QK_ERR_CUDA, "D2H(flags)");
+    }
+    if (flags & 1u) non_finite.store(true);
+    if (ss != QK_OK) abort_all.store(true);  // no shard writes back
+    // Every shard validated before anything reaches `out` (nonlin.cpp:176-180).
+    sync_point.arrive_and_wait();
+    if (ss != QK_OK) return ss;
+    if (non_finite.load()) return fail(QK_ERR_NON_FINITE, "softmax: non-finite input");
+    if (abort_all.load()) return fail(QK_ERR_CUDA, "softmax: aborted (another device failed)");
+    if (!out_dev) {
+      ci = 0;
+      for (size_t r0 = 0; r0 < nrows; r0 += chunk_rows, ++ci) {
+        const size_t cr = std::min(chunk_rows, nrows - r0);
+        QK_CUDA(cudaMemcpyAsync(out + (rb + r0) * cols, st.d_out + r0 * cols,
+                                cr * cols * sizeof(float), cudaMemcpyDeviceToHost,
+                                st.streams[ci % 3]),
+                "D2H");
+      }
+      for (auto& str : st.streams) QK_CUDA(cudaStreamSynchronize(str), "stream sync");
+    }
+    return QK_OK;
+  });
+  if (non_finite.load() && (s == QK_OK || s == QK_ERR_NON_FINITE)) {
+    return fail(QK_ERR_NON_FINITE, "softmax: non-finite input");
+  }
+  return s;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int qk_abi_version(void) { return QK_ABI_VERSION; }
+const char* qk_last_error(void) { return g_error.c_str(); }
+int qk_is_invalid_argument(qk_status s) { return s >= 1 && s < 100 ? 1 : 0; }
+
+qk_status qk_device_count(int* count) {
+  if (!count) return fail(QK_ERR_BAD_ARGUMENT, "device_count: null pointer");
+  const cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return QK_OK;
+}
+
+qk_status qk_set_devices(const int* devices, int n) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+  std::vector<int> v;
+  for (int i = 0; i < n; ++i) {
+    if (devices[i] < 0 || devices[i] >= count || devices[i] >= kMaxDevices) {
+      return fail(QK_ERR_NO_DEVICE, "set_devices: no such device");
+    }
+    if (std::find(v.begin(), v.end(), devices[i]) != v.end()) {
+      return fail(QK_ERR_BAD_ARGUMENT, "set_devices: duplicate device");
+    }
+    v.push_back(devices[i]);
+  }
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  g_devices = v;
+  return QK_OK;
+}
+
+int qk_get_devices(int* devices, int cap) {
+  const std::vector<int> v = active_devices();
+  for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) devices[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
+void qk_release_workspace(void) {
+  int prev = current_device();
+  for (int d = 0; d < kMaxDevices; ++d) {
+    DeviceState& st = g_state[d];
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (st.streams[0] == nullptr && st.d_in == nullptr) continue;
+    cudaSetDevice(d);
+    if (st.d_in) cudaFree(st.d_in);
+    if (st.d_out) cudaFree(st.d_out);
+    if (st.d_flags) cudaFree(st.d_flags);
+    for (auto& s : st.streams) {
+      if (s) cudaStreamDestroy(s);
+      s = nullptr;
+    }
+    st.d_in = st.d_out = nullptr;
+    st.d_flags = nullptr;
+    st.cap = 0;
+  }
+  cudaSetDevice(prev);
+}
+
+// ---- coefficients ----
+qk_status qk_coeffs_for(float p, float q, int32_t bias, qk_affine_coeffs* out) {
+  if (!out) return fail(QK_ERR_BAD_ARGUMENT, "coeffs_for: null pointer");
+  if (p == 0.0f) return fail(QK_ERR_ZERO_SLOPE, "coeffs_for: input scale p must be non-zero");
+  *out = make_coeffs(p, q, bias != 0);
+  return QK_OK;
+}
+qk_affine_coeffs qk_natural_exp_coeffs(int32_t bias) {
+  return make_coeffs(static_cast<float>(kLog2e), 0.0f, bias != 0);  // kernels.cpp:42-45
+}
+qk_affine_coeffs qk_base2_coeffs(int32_t bias) { return make_coeffs(1.0f, 0.0f, bias != 0); }
+qk_affine_coeffs qk_negated_natural_exp_coeffs(int32_t bias) {
+  return make_coeffs(static_cast<float>(-kLog2e), 0.0f, bias != 0);  // kernels.cpp:51-54
+}
+qk_status qk_default_clamp(float p, float q, qk_clamp_range* out) {
+  if (!out) return fail(QK_ERR_BAD_ARGUMENT, "default_clamp: null pointer");
+  if (p == 0.0f) return fail(QK_ERR_ZERO_SLOPE, "default_clamp: input scale p must be non-zero");
+  // kernels.cpp:74-82
+  *out = solve_clamp(kScale * static_cast<double>(p),
+                     kScale * (static_cast<double>(127) + static_cast<double>(q)));
+  return QK_OK;
+}
+qk_clamp_range qk_clamp_for(const qk_affine_coeffs* c) {
+  return solve_clamp(static_cast<double>(c->c0), static_cast<double>(c->c1));
+}
+qk_quad_coeffs qk_quad_continuity(void) { return {1.0f / 3.0f, 0.0f, 2.0f / 3.0f}; }
+qk_quad_coeffs qk_quad_minimax(void) { return {0.33f, -0.017f, 0.68f}; }
+int qk_quad_is_continuity_default(const qk_quad_coeffs* a) { return is_continuity(*a) ? 1 : 0; }
+qk_gelu_constants qk_gelu_constants_defaults(void) { return gelu_defaults(); }
+int32_t qk_resolve_centering_bias(qk_kernel k, int32_t requested) {
+  return resolve_bias(k, requested) ? 1 : 0;
+}
+const char* qk_kernel_name(qk_kernel k) {
+  switch (k) {  // nonlin.cpp:120-130
+    case QK_EXACT: return "exact";
+    case QK_QUAKE: return "quake";
+    case QK_QUAKE2: return "quake2";
+    case QK_EXPF: return "expf";
+    case QK_FAST_EXP: return "fast_expf";
+  }
+  return "unknown";
+}
+qk_status qk_softmax_plan(size_t cols, int32_t aligned, qk_softmax_plan_info* out) {
+  if (!out) return fail(QK_ERR_BAD_ARGUMENT, "softmax_plan: null pointer");
+  const qk::SmPlan p = qk::plan_softmax(cols, aligned != 0, current_device());
+  out->variant = static_cast<int32_t>(p.variant);
+  out->width = p.width;
+  out->lanes = p.lanes;
+  out->cluster = p.cluster;
+  out->slice = p.slice;
+  out->threads = p.threads;
+  out->vpt = p.vpt;
+  out->smem = static_cast<int64_t>(p.smem);
+  return QK_OK;
+}
+
+// ---- host-span operators ----
+qk_status qk_quake_buffer(const float* xs, size_t n, float* out, size_t out_n,
+                          const qk_affine_coeffs* c, const qk_clamp_range* r) {
+  if (out_n != n) return fail(QK_ERR_SIZE_MISMATCH, "quake_buffer: output size mismatch");
+  if (!c || !r || (n && (!xs || !out))) return fail(QK_ERR_BAD_ARGUMENT, "quake_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kQuake, QK_QUAKE, -1, c, r, nullptr, &spec);
+  return s != QK_OK ? s : run_elementwise_host(spec, xs, out, n);
+}
+
+qk_status qk_quake2_buffer(const float* xs, size_t n, float* out, size_t out_n,
+                           const qk_affine_coeffs* c, const qk_quad_coeffs* a,
+                           const qk_clamp_range* r) {
+  if (out_n != n) return fail(QK_ERR_SIZE_MISMATCH, "quake2_buffer: output size mismatch");
+  if (!c || !r || !a || (n && (!xs || !out))) {
+    return fail(QK_ERR_BAD_ARGUMENT, "quake2_buffer: null pointer");
+  }
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kQuake2, QK_QUAKE2, -1, c, r, a, &spec);
+  return s != QK_OK ? s : run_elementwise_host(spec, xs, out, n);
+}
+
+qk_status qk_logistic_buffer(const float* xs, size_t n, float* out, size_t out_n, qk_kernel k,
+                             int32_t bias) {
+  if (out_n != n) return fail(QK_ERR_SIZE_MISMATCH, "logistic_buffer: output size mismatch");
+  if (n && (!xs || !out)) return fail(QK_ERR_BAD_ARGUMENT, "logistic_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kLogistic, k, bias, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : run_elementwise_host(spec, xs, out, n);
+}
+
+qk_status qk_gelu_buffer(const float* xs, size_t n, float* out, size_t out_n, qk_kernel k,
+                         int32_t bias) {
+  if (out_n != n) return fail(QK_ERR_SIZE_MISMATCH, "gelu_buffer: output size mismatch");
+  if (n && (!xs || !out)) return fail(QK_ERR_BAD_ARGUMENT, "gelu_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kGelu, k, bias, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : run_elementwise_host(spec, xs, out, n);
+}
+
+qk_status qk_exp_buffer(const float* xs, size_t n, float* out, size_t out_n, qk_kernel k) {
+  if (out_n != n) return fail(QK_ERR_SIZE_MISMATCH, "exp_buffer: output size mismatch");
+  if (n && (!xs || !out)) return fail(QK_ERR_BAD_ARGUMENT, "exp_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kExp, k, -1, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : run_elementwise_host(spec, xs, out, n);
+}
+
+qk_status qk_softmax_rows(const float* matrix, size_t n, size_t cols,
+                          const qk_softmax_params* prm, qk_kernel k, float* out, size_t out_n) {
+  if (!prm) return fail(QK_ERR_BAD_ARGUMENT, "softmax_rows: null params");
+  qk_status s = validate_sm("softmax_rows", n, cols, prm, out_n, false);
+  if (s != QK_OK) return s;
+  if (n && (!matrix || !out)) return fail(QK_ERR_BAD_ARGUMENT, "softmax_rows: null pointer");
+  return run_softmax_host(matrix, n, cols, prm, k, out);
+}
+
+qk_status qk_softmax_row(const float* v, size_t n, const qk_softmax_params* prm, qk_kernel k,
+                         float* out, size_t out_n) {
+  if (!prm) return fail(QK_ERR_BAD_ARGUMENT, "softmax_row: null params");
+  qk_status s = validate_sm("softmax_row", n, n, prm, out_n, true);
+  if (s != QK_OK) return s;
+  if (!v || !out) return fail(QK_ERR_BAD_ARGUMENT, "softmax_row: null pointer");
+  return run_softmax_host(v, n, n, prm, k, out);
+}
+
+// ---- device operators ----
+static qk_status launch_ew_device(const EwSpec& spec, const float* xs, float* out, size_t n,
+                                  qk_stream stream) {
+  const cudaError_t e = qk::launch_elementwise(spec.op, xs, out, n, spec.p,
+                                               sm_count_of(current_device()),
+                                               reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? QK_OK : cuda_fail(e, "elementwise kernel launch");
+}
+
+qk_status qk_quake_buffer_device(const float* xs, float* out, size_t n, const qk_affine_coeffs* c,
+                                 const qk_clamp_range* r, qk_stream stream) {
+  if (!c || !r || (n && (!xs || !out))) return fail(QK_ERR_BAD_ARGUMENT, "quake_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kQuake, QK_QUAKE, -1, c, r, nullptr, &spec);
+  return s != QK_OK ? s : launch_ew_device(spec, xs, out, n, stream);
+}
+
+qk_status qk_quake2_buffer_device(const float* xs, float* out, size_t n, const qk_affine_coeffs* c,
+                                  const qk_quad_coeffs* a, const qk_clamp_range* r,
+                                  qk_stream stream) {
+  if (!c || !r || !a || (n && (!xs || !out))) {
+    return fail(QK_ERR_BAD_ARGUMENT, "quake2_buffer: null pointer");
+  }
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kQuake2, QK_QUAKE2, -1, c, r, a, &spec);
+  return s != QK_OK ? s : launch_ew_device(spec, xs, out, n, stream);
+}
+
+qk_status qk_logistic_buffer_device(const float* xs, float* out, size_t n, qk_kernel k,
+                                    int32_t bias, qk_stream stream) {
+  if (n && (!xs || !out)) return fail(QK_ERR_BAD_ARGUMENT, "logistic_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kLogistic, k, bias, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : launch_ew_device(spec, xs, out, n, stream);
+}
+
+qk_status qk_gelu_buffer_device(const float* xs, float* out, size_t n, qk_kernel k, int32_t bias,
+                                qk_stream stream) {
+  if (n && (!xs || !out)) return fail(QK_ERR_BAD_ARGUMENT, "gelu_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kGelu, k, bias, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : launch_ew_device(spec, xs, out, n, stream);
+}
+
+qk_status qk_exp_buffer_device(const float* xs, float* out, size_t n, qk_kernel k,
+                               qk_stream stream) {
+  if (n && (!xs || !out)) return fail(QK_ERR_BAD_ARGUMENT, "exp_buffer: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kExp, k, -1, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : launch_ew_device(spec, xs, out, n, stream);
+}
+
+qk_status qk_softmax_rows_device(const float* matrix, size_t n, size_t cols,
+                                 const qk_softmax_params* prm, qk_kernel k, float* out,
+                                 uint32_t* d_flags, qk_stream stream) {
+  if (!prm) return fail(QK_ERR_BAD_ARGUMENT, "softmax_rows: null params");
+  qk_status s = validate_sm("softmax_rows", n, cols, prm, n, false);
+  if (s != QK_OK) return s;
+  if (n && (!matrix || !out)) return fail(QK_ERR_BAD_ARGUMENT, "softmax_rows: null pointer");
+  qk::SmKernel sk;
+  qk::SmParams sp;
+  s = resolve_sm(prm, k, &sk, &sp);
+  if (s != QK_OK) return s;
+  const size_t rows = n / cols;
+  const qk::SmPlan plan =
+      qk::plan_softmax(cols, aligned16(matrix) && aligned16(out), current_device());
+  const cudaError_t e = qk::launch_softmax(sk, plan, matrix, out, rows, cols, sp, d_flags,
+                                           reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? QK_OK : cuda_fail(e, "softmax kernel launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Internal launch interface between the C++ host layer (host_api.cpp) and
+// the sm_100a kernels (elementwise.cu, softmax.cu). Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace qk {
+
+// Elementwise operator families (one templated kernel per family).
+enum class EwOp : int {
+  kQuake = 0,         // kernels.cpp:95-107 quake_buffer
+  kQuake2 = 1,        // kernels.cpp:109-136 quake2_buffer, continuity quad
+  kQuake2General = 2, // quake2_buffer, any other quad (refine_general)
+  kExpExpf = 3,       // comparison: expf(x), identical structure
+  kExpFast = 4,       // comparison: __expf(x)
+  kLogisticQuake = 5, // nonlin.cpp:225-233
+  kLogisticQuake2 = 6,// nonlin.cpp:234-242
+  kLogisticExpf = 7,  // nonlin.cpp:215-221 (Exact)
+  kLogisticFast = 8,  // comparison: __expf
+  kGeluQuake = 9,     // nonlin.cpp:310-319
+  kGeluQuake2 = 10,   // nonlin.cpp:320-329
+  kGeluTanh = 11,     // nonlin.cpp:298-306 (Exact, tanh form)
+  kGeluExpf = 12,     // comparison: sigmoid form with expf
+  kGeluFast = 13,     // comparison: sigmoid form with __expf
+};
+
+struct EwParams {
+  float c0, c1;          // fused affine coefficients
+  float lo, hi;          // saturation range
+  float a0, a1, a2;      // quad coefficients (kQuake2General)
+  float k0, k1, k2;      // op constants (GELU: inverse_kappa / kappa / root2_over_pi)
+  int x86_overflow;      // 1: emulate cvttss2si out-of-range semantics
+};
+
+// Launch the elementwise kernel for `op` over n floats. No allocation, no
+// synchronisation. `sm_count` sizes the persistent grid.
+cudaError_t launch_elementwise(EwOp op, const float* in, float* out, size_t n,
+                               const EwParams& p, int sm_count, cudaStream_t stream);
+
+// ---- row softmax ----
+
+enum class SmKernel : int { kExact = 0, kQuake = 1, kQuake2 = 2, kQuake2General = 3,
+                            kExpf = 4, kFast = 5 };
+
+// Reduction geometry of one launch (also reported through qk_softmax_plan so
+// the tests can restate the exact summation order).
+enum class SmVariant : int {
+  kWarpVec = 0,     // warp per row, row in registers, float4 lanes
+  kWarpScalar = 1,  // warp per row, row in registers, scalar lanes
+  kSmem = 2,        // CTA (or cluster of CTAs) per row, row staged in smem
+  kGlobal3 = 3,     // CTA per row, three sweeps over global memory (huge rows)
+};
+
+struct SmPlan {
+  SmVariant variant;
+  int width;        // elements per lane access (4 = float4, 1 = scalar)
+  int lanes;        // threads contributing partial sums per CTA (tree size)
+  int cluster;      // CTAs per row (1 = no cluster)
+  long long slice;  // chunks (of `width` elements) per CTA slice; 0 = whole row
+  int vpt;          // warp variants: chunks held per lane
+  int threads;      // CTA size
+  size_t smem;      // dynamic shared memory per CTA (bytes)
+};
+
+struct SmParams {
+  float t;          // temperature (Exact paths)
+  float c0;         // RN(2^23 * t * log2e)          nonlin.cpp:89
+  double c1_base;   // 2^23 * (127 - beta)           nonlin.cpp:90-91
+  double vmin_off;  // 126 * ln2 / t                 nonlin.cpp:92-93
+  float a0, a1, a2; // quad (kQuake2General)
+};
+
+SmPlan plan_softmax(size_t cols, bool aligned16, int device);
+
+// Launch softmax over `rows` rows of `cols` columns. `flags` (device, may be
+// null) receives bit 0 when a non-finite input was seen.
+cudaError_t launch_softmax(SmKernel k, const SmPlan& plan, const float* in, float* out,
+                           size_t rows, size_t cols, const SmParams& p, uint32_t* flags,
+                           cudaStream_t stream);
+
+}  // namespace qk

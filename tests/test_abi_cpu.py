@@ -1,0 +1,162 @@
+"""CPU: the C-ABI library loads, exports every declared symbol, and its host
+logic (coefficient derivation, validation order and messages, launch
+planning) matches the reference — no GPU needed for any of this."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2412_00408_b200 as qk
+from paper_2412_00408_b200 import _lib
+from oracle.oracle import CONTINUITY
+from tests.helpers import bits, restatement
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "quake_b200.h")
+LOG2E = np.float32(1.4426950408889634)
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qk_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(line.split()[-1] for line in out.splitlines() if line.strip())
+    decl = declared_functions()
+    assert len(decl) >= 33
+    missing = [d for d in decl if d not in exported]
+    assert not missing, missing
+    # the ctypes binding covers the whole header
+    assert set(decl) == set(_lib.SIGNATURES), set(decl) ^ set(_lib.SIGNATURES)
+
+
+def test_abi_version_and_loud_failure(tmp_path, monkeypatch):
+    assert qk.lib().qk_abi_version() == _lib.ABI_VERSION
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(_lib, "_LIB", None)
+    with pytest.raises(_lib.QuakeLibraryMissing):
+        _lib.lib()
+
+
+def test_no_oracle_in_product_package():
+    pkg = os.path.join(ROOT, "paper_2412_00408_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                text = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "oracle.oracle" not in text and "liboracle" not in text, f
+                assert "libquake_ref" not in text, f
+
+
+@pytest.mark.parametrize("p,q", [(LOG2E, 0.0), (-LOG2E, 0.0), (1.0, 0.0), (0.7, 0.37),
+                                 (np.float32(-0.10309318), 0.0), (3.0, -2.5)])
+@pytest.mark.parametrize("bias", [False, True])
+def test_coefficients_match_oracle(p, q, bias):
+    R = restatement()
+    c = qk.coeffs_for(p, q, bias)
+    assert (c.c0, c.c1) == R.coeffs_for(p, q, bias)
+    r = qk.clamp_for(c)
+    assert (r.lo, r.hi) == R.clamp_for(c.c0, c.c1)
+    d = qk.default_clamp(p, q)
+    assert (d.lo, d.hi) == R.default_clamp(p, q)
+
+
+def test_named_coefficients_and_constants():
+    R = restatement()
+    assert (qk.natural_exp_coeffs(True).c0, qk.natural_exp_coeffs(True).c1) == R.coeffs_for(LOG2E, 0, 1)
+    assert (qk.negated_natural_exp_coeffs(False).c0,
+            qk.negated_natural_exp_coeffs(False).c1) == R.coeffs_for(-LOG2E, 0, 0)
+    assert (qk.base2_coeffs().c0, qk.base2_coeffs().c1) == (8388608.0, 1065353216.0)
+    g = qk.GeluConstants.defaults()
+    assert (g.kappa, g.root2_over_pi, g.fused_scale, g.inverse_kappa) == R.gelu_constants()
+    cq = qk.QuadCoeffs.continuity()
+    assert (cq.a0, cq.a1, cq.a2) == CONTINUITY and cq.is_continuity_default()
+    assert not qk.QuadCoeffs.minimax().is_continuity_default()
+    assert qk.QuadCoeffs(np.float32(1 / 3), np.float32(-0.0), np.float32(2 / 3)).is_continuity_default()
+    assert qk.resolve_centering_bias(qk.KernelChoice.Quake, None)
+    assert not qk.resolve_centering_bias(qk.KernelChoice.Quake2, None)
+    assert qk.resolve_centering_bias(qk.KernelChoice.Quake2, True)
+    assert [qk.kernel_name(k) for k in (0, 1, 2)] == ["exact", "quake", "quake2"]
+
+
+def test_validation_errors_match_reference_messages():
+    """Precondition order and messages of kernels.cpp / nonlin.cpp (no GPU reached)."""
+    K = qk.KernelChoice
+    x = np.zeros(8, np.float32)
+    c = qk.natural_exp_coeffs(True)
+    r = qk.clamp_for(c)
+    cases = [
+        (lambda: qk.quake_buffer(x, np.zeros(7, np.float32), c, r), "quake_buffer: output size mismatch"),
+        (lambda: qk.quake2_buffer(x, np.zeros(9, np.float32), c, qk.QuadCoeffs.continuity(), r),
+         "quake2_buffer: output size mismatch"),
+        (lambda: qk.logistic_buffer(x, np.zeros(1, np.float32), K.Quake),
+         "logistic_buffer: output size mismatch"),
+        (lambda: qk.gelu_buffer(x, np.zeros(1, np.float32), K.Quake2), "gelu_buffer: output size mismatch"),
+        (lambda: qk.softmax_rows(np.zeros(5, np.float32), 2, qk.SoftmaxParams(), K.Quake),
+         "softmax_rows: length not divisible by cols"),
+        (lambda: qk.softmax_rows(x, 0, qk.SoftmaxParams(), K.Quake),
+         "softmax_rows: length not divisible by cols"),
+        (lambda: qk.softmax_rows(x, 4, qk.SoftmaxParams(), K.Quake, out=np.zeros(4, np.float32)),
+         "softmax_rows: output size mismatch"),
+        (lambda: qk.softmax_rows(x, 4, qk.SoftmaxParams(temperature=0.0), K.Quake),
+         "softmax_rows: temperature must be positive"),
+        (lambda: qk.softmax_rows(x, 4, qk.SoftmaxParams(temperature=float("nan")), K.Quake),
+         "softmax_rows: temperature must be positive"),
+        (lambda: qk.softmax_row(np.zeros(0, np.float32), qk.SoftmaxParams(), K.Exact),
+         "softmax: empty row"),
+        (lambda: qk.softmax_row(x, qk.SoftmaxParams(temperature=-1.0), K.Exact),
+         "softmax_row: temperature must be positive"),
+        (lambda: qk.softmax_row(x, qk.SoftmaxParams(), K.Exact, out=np.zeros(3, np.float32)),
+         "softmax_row: output size mismatch"),
+        (lambda: qk.coeffs_for(0.0, 1.0), "coeffs_for: input scale p must be non-zero"),
+        (lambda: qk.default_clamp(0.0, 0.0), "default_clamp: input scale p must be non-zero"),
+    ]
+    for fn, msg in cases:
+        with pytest.raises(qk.QuakeInvalidArgument) as ei:
+            fn()
+        assert str(ei.value) == msg
+        assert isinstance(ei.value, ValueError)
+
+
+def test_empty_inputs_are_noops():
+    """Empty buffers and an empty matrix are valid (kernels.cpp:95-107, nonlin.cpp:162-189)."""
+    K = qk.KernelChoice
+    e = np.zeros(0, np.float32)
+    c = qk.natural_exp_coeffs(True)
+    assert qk.quake_buffer(e, c, qk.clamp_for(c)).size == 0
+    assert qk.logistic_buffer(e, K.Quake).size == 0
+    assert qk.softmax_rows(e, 4, qk.SoftmaxParams(), K.Quake2).size == 0
+
+
+def test_softmax_plan_geometry():
+    p = qk.softmax_plan(512)
+    assert (p["variant"], p["width"], p["lanes"], p["vpt"]) == (0, 4, 32, 4)
+    p = qk.softmax_plan(128256)
+    assert (p["variant"], p["cluster"], p["slice"], p["threads"]) == (2, 8, 4008, 512)
+    assert p["smem"] == 4008 * 16
+    p = qk.softmax_plan(513, False)
+    assert (p["variant"], p["width"]) == (1, 1)
+    p = qk.softmax_plan(300000)
+    assert p["variant"] == 2 and p["cluster"] == 16
+    p = qk.softmax_plan(1 << 23)
+    assert p["variant"] == 3
+    for cols in (1025, 5000, 65536, 128256, 600000):
+        p = qk.softmax_plan(cols)
+        if p["variant"] == 2:
+            assert p["slice"] * p["cluster"] * p["width"] >= cols
+            assert p["smem"] <= 227 * 1024
+
+
+def test_cuda_calls_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    K = qk.KernelChoice
+    with pytest.raises(qk.QuakeCudaError):
+        qk.logistic_buffer(np.ones(16, np.float32), K.Quake)
