@@ -96,7 +96,8 @@ typedef struct {
 /* Softmax launch plan (introspection; the reduction geometry that fixes the
  * summation order, see softmax.cu). */
 typedef struct {
-  int32_t variant; /* 0 warp/float4, 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep */
+  int32_t variant; /* 0 warp/float4, 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep,
+                      4 persistent TMA pipeline (+cluster) */
   int32_t width;   /* elements per chunk: 4 or 1 */
   int32_t lanes;   /* partial-sum lanes per CTA */
   int32_t cluster; /* CTAs per row */
@@ -104,6 +105,9 @@ typedef struct {
   int32_t threads; /* CTA size */
   int32_t vpt;     /* warp variants: chunks per lane */
   int64_t smem;    /* dynamic smem bytes per CTA */
+  int32_t stages;  /* variant 4: row slices in flight per CTA */
+  int32_t balanced;/* 1: CTA r's slice is q (+1 for r < nchunks % cluster) chunks;
+                      0: `slice` chunks per CTA, the last one short */
 } qk_softmax_plan_info;
 
 /* ---- library ---- */

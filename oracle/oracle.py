@@ -68,7 +68,7 @@ class Restatement:
                                       c_float, c_int, c_int, _fp]
         L.or_softmax_rows_ordered.argtypes = [_fp, c_size_t, c_size_t, c_float, c_int, c_float,
                                               c_float, c_float, c_int, c_int, c_int, c_int,
-                                              ctypes.c_longlong, _fp]
+                                              ctypes.c_longlong, c_int, _fp]
         L.or_softmax_row_scalars.argtypes = [c_float, c_float, c_int, _fp, _fp, _fp]
         L.or_gelu_constants.argtypes = [_fp] * 4
         for name in ("or_exact_exp", "or_exact_logistic", "or_exact_gelu_tanh",
@@ -155,7 +155,8 @@ class Restatement:
         out = np.empty_like(m)
         st = self.lib.or_softmax_rows_ordered(_ptr(m), m.size, cols, temperature, bias, *quad,
                                               kernel, plan["width"], plan["lanes"],
-                                              plan["cluster"], plan["slice"], _ptr(out))
+                                              plan["cluster"], plan["slice"],
+                                              int(plan.get("balanced", 0)), _ptr(out))
         if st != 0:
             raise OracleError(f"softmax_rows_ordered status {st}")
         return out

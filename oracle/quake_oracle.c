@@ -264,24 +264,36 @@ int or_softmax_rows(const float* mat, size_t n, size_t cols, float temperature,
   return OR_OK;
 }
 
-/* Butterfly over `lanes` partials in the GPU kernels' mask order; returns
- * lane 0's value (every lane ends equal since fp addition commutes). */
-static float butterfly_sum(float* p, int lanes) {
+/* Block tree of the GPU kernels over `lanes` thread partials (lanes = 32 for
+ * the warp kernels, else a multiple of 32): butterfly with xor masks
+ * 16,8,4,2,1 inside each warp; then lane 0's value of each warp, padded with
+ * +0.0 up to the next power of two P, butterfly with masks P/2..1; returns
+ * element 0 (every lane ends equal since fp addition commutes). */
+static float block_tree_sum(float* p, int lanes) {
   float tmp[1024];
-  int masks[16], nm = 0;
-  for (int o = (lanes < 32 ? lanes : 32) / 2; o > 0; o >>= 1) masks[nm++] = o;
-  for (int o = lanes / 2; o >= 32; o >>= 1) masks[nm++] = o;
-  for (int k = 0; k < nm; ++k) {
-    for (int l = 0; l < lanes; ++l) tmp[l] = p[l] + p[l ^ masks[k]];
+  const int w = lanes < 32 ? lanes : 32;
+  for (int o = w / 2; o > 0; o >>= 1) {
+    for (int l = 0; l < lanes; ++l) tmp[l] = p[l] + p[l ^ o];
     memcpy(p, tmp, sizeof(float) * (size_t)lanes);
   }
-  return p[0];
+  if (lanes <= 32) return p[0];
+  const int nw = lanes / 32;
+  int P = 1;
+  while (P < nw) P <<= 1;
+  float wv[32];
+  for (int i = 0; i < P; ++i) wv[i] = i < nw ? p[32 * i] : 0.0f;
+  for (int o = P / 2; o > 0; o >>= 1) {
+    float t2[32];
+    for (int i = 0; i < P; ++i) t2[i] = wv[i] + wv[i ^ o];
+    memcpy(wv, t2, sizeof(float) * (size_t)P);
+  }
+  return wv[0];
 }
 
 int or_softmax_rows_ordered(const float* mat, size_t n, size_t cols, float temperature,
                             int bias_req, float a0, float a1, float a2, int kernel,
                             int width, int lanes, int cluster, long long slice,
-                            float* out) {
+                            int balanced, float* out) {
   if (cols == 0 || n % cols != 0) return OR_ERR_NOT_DIVISIBLE;
   if (!(temperature > 0.0f)) return OR_ERR_BAD_TEMPERATURE;
   if (kernel == OR_EXACT || lanes > 1024 || lanes < 1) return OR_ERR_SIZE_MISMATCH;
@@ -293,7 +305,7 @@ int or_softmax_rows_ordered(const float* mat, size_t n, size_t cols, float tempe
   }
   const int general = !is_continuity(a0, a1, a2);
   const long long nchunks = (long long)(cols / (size_t)width);
-  if (slice <= 0) { slice = nchunks; cluster = 1; }
+  if (slice <= 0) { slice = nchunks; cluster = 1; balanced = 0; }
   float part[1024];
   for (size_t r = 0; r < rows; ++r) {
     const float* v = mat + r * cols;
@@ -307,11 +319,18 @@ int or_softmax_rows_ordered(const float* mat, size_t n, size_t cols, float tempe
                                 : quake2_body(u, c0, c1, general, a0, a1, a2);
     }
     float S = 0.0f;
+    const long long q = nchunks / cluster, rem = nchunks % cluster;
     for (int c = 0; c < cluster; ++c) {
-      const long long b = (long long)c * slice;
-      long long cnt = nchunks - b;
-      if (cnt > slice) cnt = slice;
-      if (cnt < 0) cnt = 0;
+      long long b, cnt;
+      if (balanced) {  /* rank c: q (+1 for the first rem ranks) chunks */
+        b = (long long)c * q + (c < rem ? c : rem);
+        cnt = q + (c < rem ? 1 : 0);
+      } else {         /* rank c: `slice` chunks, the last one short */
+        b = (long long)c * slice;
+        cnt = nchunks - b;
+        if (cnt > slice) cnt = slice;
+        if (cnt < 0) cnt = 0;
+      }
       for (int l = 0; l < lanes; ++l) {
         float s = 0.0f;
         for (long long j = l; j < cnt; j += lanes) {
@@ -319,7 +338,7 @@ int or_softmax_rows_ordered(const float* mat, size_t n, size_t cols, float tempe
         }
         part[l] = s;
       }
-      const float cs = butterfly_sum(part, lanes);
+      const float cs = block_tree_sum(part, lanes);
       S = c == 0 ? cs : S + cs;
     }
     for (size_t i = 0; i < cols; ++i) y[i] = y[i] / S;

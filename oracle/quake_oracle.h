@@ -70,16 +70,18 @@ int or_softmax_rows(const float* m, size_t n, size_t cols, float temperature,
 
 /* Same arithmetic as or_softmax_rows (QuAKE kernels only), but each row is
  * summed in the declared order of the GPU kernels (paper_2412_00408_b200/
- * csrc/softmax.cu): the row is cut into `cluster` slices of `slice` chunks
- * (slice 0 = one slice), a chunk being `width` consecutive elements; lane l
- * of `lanes` adds the elements of chunks l, l+lanes, ... of its slice in
- * index order; lanes combine by butterfly with xor masks 16,8,4,2,1 then
- * lanes/2, ..., 32; slice partials are added sequentially in slice order.
- * Only the reference's sequential fp32 sum (nonlin.cpp:63-67) is replaced. */
+ * csrc/softmax.cu): the row (in chunks of `width` consecutive elements) is
+ * cut into `cluster` slices — `balanced`: the first nchunks % cluster slices
+ * get one extra chunk; else `slice` chunks each, the last short; slice 0 =
+ * one slice. Lane l of `lanes` adds the elements of chunks l, l+lanes, ... of
+ * its slice in index order; lanes combine by butterfly (xor 16..1 inside a
+ * warp, then over warp results zero-padded to a power of two); slice
+ * partials are added sequentially in slice order. Only the reference's
+ * sequential fp32 sum (nonlin.cpp:63-67) is replaced. */
 int or_softmax_rows_ordered(const float* m, size_t n, size_t cols, float temperature,
                             int bias, float a0, float a1, float a2, int kernel,
                             int width, int lanes, int cluster, long long slice,
-                            float* out);
+                            int balanced, float* out);
 
 /* Per-row scalars of the fused softmax (nonlin.cpp:85-93), exposed so tests
  * can pin the device's fp64 derivation. */

@@ -324,6 +324,7 @@ qk_status resolve_sm(const qk_softmax_params* prm, qk_kernel k, qk::SmKernel* sk
         *sk = qk::SmKernel::kQuake2;
       } else {
         *sk = qk::SmKernel::kQuake2General;
+        p.general_quad = 1;
         p.a0 = prm->quad.a0;
         p.a1 = prm->quad.a1;
         p.a2 = prm->quad.a2;
@@ -663,6 +664,8 @@ qk_status qk_softmax_plan(size_t cols, int32_t aligned, qk_softmax_plan_info* ou
   out->threads = p.threads;
   out->vpt = p.vpt;
   out->smem = static_cast<int64_t>(p.smem);
+  out->stages = p.stages;
+  out->balanced = p.balanced;
   return QK_OK;
 }
 

@@ -52,6 +52,7 @@ enum class SmVariant : int {
   kWarpScalar = 1,  // warp per row, row in registers, scalar lanes
   kSmem = 2,        // CTA (or cluster of CTAs) per row, row staged in smem
   kGlobal3 = 3,     // CTA per row, three sweeps over global memory (huge rows)
+  kPipe = 4,        // persistent cluster per row group, multi-stage TMA pipeline
 };
 
 struct SmPlan {
@@ -63,6 +64,8 @@ struct SmPlan {
   int vpt;          // warp variants: chunks held per lane
   int threads;      // CTA size
   size_t smem;      // dynamic shared memory per CTA (bytes)
+  int stages;       // kPipe: row slices in flight per CTA
+  int balanced;     // kPipe: rank r owns q (+1 if r < nchunks % cluster) chunks
 };
 
 struct SmParams {
@@ -71,6 +74,7 @@ struct SmParams {
   double c1_base;   // 2^23 * (127 - beta)           nonlin.cpp:90-91
   double vmin_off;  // 126 * ln2 / t                 nonlin.cpp:92-93
   float a0, a1, a2; // quad (kQuake2General)
+  int general_quad; // 1: y_m may leave [1, 2]; rows use SSE-exact semantics
 };
 
 SmPlan plan_softmax(size_t cols, bool aligned16, int device);

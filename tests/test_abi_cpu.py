@@ -137,16 +137,21 @@ def test_empty_inputs_are_noops():
 def test_softmax_plan_geometry():
     p = qk.softmax_plan(512)
     assert (p["variant"], p["width"], p["lanes"], p["vpt"]) == (0, 4, 32, 4)
-    p = qk.softmax_plan(128256)
-    assert (p["variant"], p["cluster"], p["slice"], p["threads"]) == (2, 8, 4008, 512)
-    assert p["smem"] == 4008 * 16
     p = qk.softmax_plan(513, False)
     assert (p["variant"], p["width"]) == (1, 1)
-    p = qk.softmax_plan(300000)
-    assert p["variant"] == 2 and p["cluster"] == 16
     p = qk.softmax_plan(1 << 23)
     assert p["variant"] == 3
-    for cols in (1025, 5000, 65536, 128256, 600000):
+    for cols in (2048, 4096, 16384, 50000, 65536, 128256, 300000):
+        p = qk.softmax_plan(cols)
+        assert p["variant"] == 4 and p["balanced"] == 1, (cols, p)
+        chunks = cols // 4
+        q, rem = divmod(chunks, p["cluster"])
+        assert p["slice"] == q + (1 if rem else 0)
+        # every thread owns KC-1 unconditional chunks, the last predicated
+        assert p["threads"] % 32 == 0 and p["threads"] <= 512
+        assert p["threads"] * (p["vpt"] - 1) <= q <= p["threads"] * p["vpt"]
+        assert p["stages"] >= 2 and p["smem"] <= 224 * 1024
+    for cols in (1025, 600000):
         p = qk.softmax_plan(cols)
         if p["variant"] == 2:
             assert p["slice"] * p["cluster"] * p["width"] >= cols
