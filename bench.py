@@ -360,6 +360,17 @@ def per_config(qk, L, _lib, peak, iters=12):
         pairs = max(2, -(-4 * l2 // (8 * n)))
         xs = [w.device() for _ in range(pairs)]
         ys = [torch.empty_like(xs[0]) for _ in range(pairs)]
+        # same harness, plain device-to-device copy of the same bytes: what
+        # a pure stream reaches at this size (launch + ramp overheads included)
+        def copy_fn(x, y):
+            def f():
+                y.copy_(x)
+                return 0
+            return f
+        sc = timeit([copy_fn(x, y) for x, y in zip(xs, ys)])
+        res[f"{w.name}:copy_reference"] = {"us": sc * 1e6, "gbps": BYTES_PER_ELEM * n / sc / 1e9,
+                                           "frac": BYTES_PER_ELEM * n / sc / 1e9 / peak,
+                                           "rotation_buffers": pairs}
         for kn in ("quake", "quake2", "expf", "fast_expf"):
             k = int({"quake": K.Quake, "quake2": K.Quake2, "expf": K.Expf,
                      "fast_expf": K.FastExp}[kn])

@@ -108,6 +108,7 @@ typedef struct {
   int32_t stages;  /* variant 4: row slices in flight per CTA */
   int32_t balanced;/* 1: CTA r's slice is q (+1 for r < nchunks % cluster) chunks;
                       0: `slice` chunks per CTA, the last one short */
+  int32_t resident;/* variant 4: clusters resident at once on this device (0 = unknown) */
 } qk_softmax_plan_info;
 
 /* ---- library ---- */

@@ -52,7 +52,7 @@ class SoftmaxPlanC(Structure):
     _fields_ = [("variant", c_int32), ("width", c_int32), ("lanes", c_int32),
                 ("cluster", c_int32), ("slice", c_int64), ("threads", c_int32),
                 ("vpt", c_int32), ("smem", c_int64), ("stages", c_int32),
-                ("balanced", c_int32)]
+                ("balanced", c_int32), ("resident", c_int32)]
 
 
 _fp = POINTER(c_float)

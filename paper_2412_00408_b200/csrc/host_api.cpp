@@ -666,6 +666,7 @@ qk_status qk_softmax_plan(size_t cols, int32_t aligned, qk_softmax_plan_info* ou
   out->smem = static_cast<int64_t>(p.smem);
   out->stages = p.stages;
   out->balanced = p.balanced;
+  out->resident = p.resident;
   return QK_OK;
 }
 

@@ -66,6 +66,7 @@ struct SmPlan {
   size_t smem;      // dynamic shared memory per CTA (bytes)
   int stages;       // kPipe: row slices in flight per CTA
   int balanced;     // kPipe: rank r owns q (+1 if r < nchunks % cluster) chunks
+  int resident;     // kPipe: clusters resident at once (occupancy API; 0 = unknown)
 };
 
 struct SmParams {

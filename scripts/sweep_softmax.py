@@ -43,12 +43,13 @@ def main():
     y = torch.empty_like(x)
     ref = None
     envs = [{}]
-    for c in (4, 5, 6, 7, 8, 9, 10, 11, 12, 16):
+    for c in (5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 16):
         envs.append({"QK_SM_CLUSTER": c})
-    for c in (6, 8, 9):
-        for kc in (8, 4):
-            envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": kc})
-    envs += [{"QK_SM_CLUSTER": 8, "QK_SM_STAGES": 2}, {"QK_SM_CLUSTER": 9, "QK_SM_STAGES": 3}]
+    for c in (9, 12, 14, 16):
+        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 8})
+    for c in (5, 6, 8, 9, 10, 11, 12, 14):
+        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 12})
+    envs += [{"QK_SM_CLUSTER": 9, "QK_SM_SMEM_KB": 112}, {"QK_SM_CLUSTER": 16, "QK_SM_SMEM_KB": 150}]
     for env in envs:
         try:
             ms, plan = time_plan(w, x, y, env)
@@ -60,7 +61,7 @@ def main():
         same = bool(torch.equal(y.view(-1)[:1000], ref.view(-1)[:1000]))
         gbs = 8 * w.n / (ms * 1e-3) / 1e9
         print(json.dumps({"env": env, "ms": round(ms, 4), "GBps": round(gbs, 1),
-                          "plan": {k: plan[k] for k in ("variant", "cluster", "threads", "stages", "slice", "vpt")},
+                          "plan": {k: plan[k] for k in ("variant", "cluster", "threads", "stages", "slice", "vpt", "resident", "smem")},
                           "first_rows_equal_default": same}), flush=True)
 
 
