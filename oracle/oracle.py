@@ -77,6 +77,9 @@ class Restatement:
             getattr(L, name).restype = c_double
         L.or_exact_softmax.argtypes = [_fp, c_size_t, c_double, _dp]
         L.or_check_div3_replacement.restype = c_uint64
+        L.or_sweep_compare.argtypes = [c_int, c_int, c_int, c_uint64, c_uint64, c_void_p, c_int,
+                                       POINTER(c_uint64)]
+        L.or_sweep_compare.restype = c_uint64
 
     # --- coefficient derivation (kernels.cpp:25-87) ---
     def coeffs_for(self, p, q=0.0, centering_bias=False):
@@ -177,6 +180,15 @@ class Restatement:
         if self.lib.or_exact_softmax(_ptr(v), v.size, t, _ptr(out, _dp)) != 0:
             raise OracleError("exact_softmax: bad shapes")
         return out
+
+    def sweep_compare(self, op, kernel, bias, start, got: np.ndarray, threads=None):
+        """Mismatches of op over bit patterns start..start+len(got)-1 vs `got`."""
+        threads = threads or max(1, os.cpu_count() or 1)
+        fb = c_uint64()
+        got = np.ascontiguousarray(got, dtype=np.float32)
+        bad = self.lib.or_sweep_compare(op, kernel, bias, start, got.size, got.ctypes.data,
+                                        threads, ctypes.byref(fb))
+        return int(bad), int(fb.value)
 
     def check_div3_replacement(self) -> int:
         return int(self.lib.or_check_div3_replacement())

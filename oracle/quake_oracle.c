@@ -6,6 +6,7 @@
 #include "quake_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <string.h>
 
 /* std::numbers::log2e / ln2 / pi as exact binary64 literals. */
@@ -385,5 +386,68 @@ uint64_t or_check_div3_replacement(void) {
     const float q1 = fmaf(res, r3, q0);
     if (f2u(q1) != f2u(t / 3.0f)) ++bad;
   }
+  return bad;
+}
+
+typedef struct {
+  int op, kernel, bias;
+  uint64_t start, count;
+  const float* got;
+  uint64_t bad, first_bad;
+} sweep_job;
+
+static void* sweep_worker(void* arg) {
+  sweep_job* j = (sweep_job*)arg;
+  enum { B = 4096 };
+  float xs[B], ys[B];
+  float c0 = 0, c1 = 0, lo = 0, hi = 0;
+  if (j->op <= 1) {
+    or_coeffs_for((float)kLog2e, 0.0f, j->bias, &c0, &c1);
+    or_clamp_for(c0, c1, &lo, &hi);
+  }
+  j->bad = 0;
+  j->first_bad = UINT64_MAX;
+  for (uint64_t off = 0; off < j->count; off += B) {
+    const uint64_t n = j->count - off < B ? j->count - off : B;
+    for (uint64_t i = 0; i < n; ++i) xs[i] = u2f((uint32_t)(j->start + off + i));
+    switch (j->op) {
+      case 0: or_quake_buffer(xs, ys, n, c0, c1, lo, hi); break;
+      case 1: or_quake2_buffer(xs, ys, n, c0, c1, 1.0f / 3.0f, 0.0f, 2.0f / 3.0f, lo, hi); break;
+      case 2: or_logistic_buffer(xs, ys, n, j->kernel, j->bias); break;
+      default: or_gelu_buffer(xs, ys, n, j->kernel, j->bias); break;
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+      if (f2u(ys[i]) != f2u(j->got[off + i])) {
+        if (j->bad == 0) j->first_bad = j->start + off + i;
+        ++j->bad;
+      }
+    }
+  }
+  return NULL;
+}
+
+uint64_t or_sweep_compare(int op, int kernel, int bias, uint64_t start, uint64_t count,
+                          const float* got, int threads, uint64_t* first_bad) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t tid[256];
+  sweep_job jobs[256];
+  const uint64_t per = (count + (uint64_t)threads - 1) / (uint64_t)threads;
+  int used = 0;
+  for (int t = 0; t < threads; ++t) {
+    const uint64_t b = (uint64_t)t * per;
+    if (b >= count) break;
+    jobs[t] = (sweep_job){op, kernel, bias, start + b, count - b < per ? count - b : per,
+                          got + b, 0, 0};
+    pthread_create(&tid[t], NULL, sweep_worker, &jobs[t]);
+    ++used;
+  }
+  uint64_t bad = 0, fb = UINT64_MAX;
+  for (int t = 0; t < used; ++t) {
+    pthread_join(tid[t], NULL);
+    bad += jobs[t].bad;
+    if (jobs[t].bad && jobs[t].first_bad < fb) fb = jobs[t].first_bad;
+  }
+  if (first_bad) *first_bad = fb;
   return bad;
 }

@@ -100,6 +100,15 @@ double or_exact_gelu_tanh(double x);
 double or_exact_gelu_sigmoid(double x);
 int or_exact_softmax(const float* v, size_t n, double temperature, double* out);
 
+/* Exhaustive sweep support: recompute op(bits = start .. start+count-1) on
+ * `threads` pthreads and compare bit-for-bit with `got` (the GPU's output for
+ * the same bit patterns). op: 0 quake_buffer, 1 quake2_buffer (continuity),
+ * 2 logistic_buffer, 3 gelu_buffer; for ops 0/1 the coefficients are the
+ * natural-exp ones with `bias`, clamp from clamp_for. Returns the number of
+ * mismatches; *first_bad receives the first mismatching bit pattern. */
+uint64_t or_sweep_compare(int op, int kernel, int bias, uint64_t start, uint64_t count,
+                          const float* got, int threads, uint64_t* first_bad);
+
 /* Exhaustive check helpers used by the CPU test-suite: returns the number of
  * fp32 values t in [3, 6] for which the reciprocal-multiply + FMA correction
  * (the device's y/3) differs from the IEEE quotient t/3. */

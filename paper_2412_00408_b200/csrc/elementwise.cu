@@ -86,12 +86,59 @@ __device__ __forceinline__ float apply(float x, const EwParams& p) {
   }
 }
 
+// Two elements of the QuAKE ops with the paired FMUL2/FFMA2 sequences of
+// numerics.cuh (bit-identical to apply<OP>); other ops go element-wise.
+template <EwOp OP, bool X86>
+__device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p) {
+  if constexpr (X86 || !(OP == EwOp::kQuake || OP == EwOp::kQuake2 ||
+                         OP == EwOp::kQuake2General || OP == EwOp::kLogisticQuake ||
+                         OP == EwOp::kLogisticQuake2 || OP == EwOp::kGeluQuake ||
+                         OP == EwOp::kGeluQuake2)) {
+    a = apply<OP, X86>(a, p);
+    b = apply<OP, X86>(b, p);
+  } else if constexpr (OP == EwOp::kGeluQuake || OP == EwOp::kGeluQuake2) {
+    // u = x * (x*x + 1/kappa): the first product is added (scalar add), the
+    // second feeds the clamp, so both products can be paired
+    float s0, s1;
+    unpack2(mul2_rn(pack2(a, b), pack2(a, b)), s0, s1);
+    float u0, u1;
+    unpack2(mul2_rn(pack2(a, b), pack2(__fadd_rn(s0, p.k0), __fadd_rn(s1, p.k0))), u0, u1);
+    u0 = saturate_fast(u0, p.lo, p.hi);
+    u1 = saturate_fast(u1, p.lo, p.hi);
+    float e0, e1;
+    if constexpr (OP == EwOp::kGeluQuake) {
+      quake_body2(u0, u1, p.c0, p.c1, e0, e1);
+    } else {
+      quake2_body2<false>(u0, u1, p.c0, p.c1, 0.f, 0.f, 0.f, e0, e1);
+    }
+    const float y0 = __fdiv_rn(a, __fadd_rn(1.0f, e0));
+    const float y1 = __fdiv_rn(b, __fadd_rn(1.0f, e1));
+    a = y0 != y0 ? x86_quiet(a) : y0;
+    b = y1 != y1 ? x86_quiet(b) : y1;
+  } else {
+    const float u0 = saturate_fast(a, p.lo, p.hi), u1 = saturate_fast(b, p.lo, p.hi);
+    float e0, e1;
+    if constexpr (OP == EwOp::kQuake || OP == EwOp::kLogisticQuake) {
+      quake_body2(u0, u1, p.c0, p.c1, e0, e1);
+    } else if constexpr (OP == EwOp::kQuake2General) {
+      quake2_body2<true>(u0, u1, p.c0, p.c1, p.a0, p.a1, p.a2, e0, e1);
+    } else {
+      quake2_body2<false>(u0, u1, p.c0, p.c1, 0.f, 0.f, 0.f, e0, e1);
+    }
+    if constexpr (OP == EwOp::kLogisticQuake || OP == EwOp::kLogisticQuake2) {
+      a = __frcp_rn(__fadd_rn(1.0f, e0));
+      b = __frcp_rn(__fadd_rn(1.0f, e1));
+    } else {
+      a = e0;
+      b = e1;
+    }
+  }
+}
+
 template <EwOp OP, bool X86>
 __device__ __forceinline__ float4 apply4(float4 v, const EwParams& p) {
-  v.x = apply<OP, X86>(v.x, p);
-  v.y = apply<OP, X86>(v.y, p);
-  v.z = apply<OP, X86>(v.z, p);
-  v.w = apply<OP, X86>(v.w, p);
+  apply2<OP, X86>(v.x, v.y, p);
+  apply2<OP, X86>(v.z, v.w, p);
   return v;
 }
 

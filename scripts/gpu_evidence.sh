@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round evidence: smoke, GPU tests, bench (both arms, torchrun path), ncu
+# launch list of the bench command, full ncu captures of the top kernels.
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv > gpurun_out/smi.csv 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference --steps 5 --warmup 2 > gpurun_out/bench_ref.log 2>&1; echo "ref exit $?" >> gpurun_out/bench_ref.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 10 --warmup 3 --no-extras > gpurun_out/bench_torchrun.log 2>&1; echo "torchrun exit $?" >> gpurun_out/bench_torchrun.log
+CMD="python bench.py --steps 3 --warmup 3 --no-extras --e2e-steps 1"
+timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:softmax_pipe -s 3 -c 1 -o gpurun_out/prof_softmax_pipe -f $CMD > gpurun_out/ncu_full.log 2>&1
+echo "ncu pipe exit $?" >> gpurun_out/ncu_full.log
+CMD2="python scripts/kernel_probe.py"
+timeout 300 $CMD2 > gpurun_out/kernel_probe.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none -k regex:"ew_vec_kernel|softmax_warp_vec" -c 3 -o /tmp/prof_ew -f $CMD2 > gpurun_out/ncu_ew.log 2>&1
+echo "ncu ew exit $?" >> gpurun_out/ncu_ew.log
+# summaries only (the full reports would exceed gpurun's 64 MiB copy-back)
+python scripts/ncu_summary.py /tmp/prof_ew.ncu-rep gpurun_out/ncu_ew_summary "elementwise + warp softmax" > /dev/null 2>&1
+python scripts/ncu_summary.py gpurun_out/prof_softmax_pipe.ncu-rep gpurun_out/ncu_pipe_summary "softmax_pipe cfg5" > /dev/null 2>&1
+du -sh gpurun_out

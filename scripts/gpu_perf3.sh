@@ -1,10 +1,10 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_softmax.py -m gpu -q --timeout 400 -rf -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 timeout 300 python scripts/sweep_softmax.py > gpurun_out/sweep.log 2>&1; echo "sweep exit $?" >> gpurun_out/sweep.log
 timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
 CMD="python bench.py --steps 2 --warmup 1 --no-extras --e2e-steps 1"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:softmax_pipe -c 1 -o gpurun_out/prof_pipe8 -f $CMD > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:softmax_pipe -c 1 -o gpurun_out/prof_pipe11 -f $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu exit $?" >> gpurun_out/ncu_full.log

@@ -47,8 +47,10 @@ def main():
         envs.append({"QK_SM_CLUSTER": c})
     for c in (9, 12, 14, 16):
         envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 8})
-    for c in (5, 6, 8, 9, 10, 11, 12, 14):
+    for c in (6, 9, 11, 12):
         envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 12})
+    for c in (7, 8, 9, 10, 11, 12):
+        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 14})
     envs += [{"QK_SM_CLUSTER": 9, "QK_SM_SMEM_KB": 112}, {"QK_SM_CLUSTER": 16, "QK_SM_SMEM_KB": 150}]
     for env in envs:
         try:
