@@ -15,7 +15,8 @@ from paper_2412_00408_b200.workloads import CONFIGS  # noqa: E402
 
 
 def time_plan(w, x, y, env, iters=10):
-    for k in ("QK_SM_CLUSTER", "QK_SM_STAGES", "QK_SM_THREADS", "QK_SM_SMEM_KB", "QK_SM_KC"):
+    for k in ("QK_SM_CLUSTER", "QK_SM_STAGES", "QK_SM_THREADS", "QK_SM_SMEM_KB", "QK_SM_KC",
+              "QK_SM_DELAY"):
         os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
     L = _lib.lib()
@@ -43,15 +44,10 @@ def main():
     y = torch.empty_like(x)
     ref = None
     envs = [{}]
-    for c in (5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 16):
-        envs.append({"QK_SM_CLUSTER": c})
-    for c in (9, 12, 14, 16):
-        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 8})
-    for c in (6, 9, 11, 12):
-        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 12})
-    for c in (7, 8, 9, 10, 11, 12):
-        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": 14})
-    envs += [{"QK_SM_CLUSTER": 9, "QK_SM_SMEM_KB": 112}, {"QK_SM_CLUSTER": 16, "QK_SM_SMEM_KB": 150}]
+    for c, kc, t in ((13, 13, 192), (13, 16, 160), (14, 15, 160), (14, 14, 192), (15, 14, 160),
+                     (15, 15, 160), (16, 16, 128), (16, 13, 160), (12, 15, 192), (11, 15, 224),
+                     (10, 14, 256), (9, 16, 224), (9, 15, 256)):
+        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": kc, "QK_SM_THREADS": t})
     for env in envs:
         try:
             ms, plan = time_plan(w, x, y, env)
