@@ -296,7 +296,9 @@ def main():
     }
     traffic = _load_traffic(w.name)
     if traffic:
-        line["roofline"]["traffic"] = traffic
+        # DRAM bytes read + written per launch, from the committed ncu capture
+        line["roofline"]["traffic"] = traffic["bytes_per_launch"]
+        line["roofline"]["traffic_source"] = traffic["source"]
     if rank == 0 and world == 1 and not args.no_extras:
         line["per_config"] = per_config(qk, L, _lib, peak)
         try:

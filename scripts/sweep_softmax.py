@@ -16,7 +16,7 @@ from paper_2412_00408_b200.workloads import CONFIGS  # noqa: E402
 
 def time_plan(w, x, y, env, iters=10):
     for k in ("QK_SM_CLUSTER", "QK_SM_STAGES", "QK_SM_THREADS", "QK_SM_SMEM_KB", "QK_SM_KC",
-              "QK_SM_DELAY"):
+              "QK_SM_DELAY", "QK_SM_POLICY"):
         os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
     L = _lib.lib()
@@ -43,11 +43,10 @@ def main():
     x = w.device()
     y = torch.empty_like(x)
     ref = None
-    envs = [{}]
-    for c, kc, t in ((13, 13, 192), (13, 16, 160), (14, 15, 160), (14, 14, 192), (15, 14, 160),
-                     (15, 15, 160), (16, 16, 128), (16, 13, 160), (12, 15, 192), (11, 15, 224),
-                     (10, 14, 256), (9, 16, 224), (9, 15, 256)):
-        envs.append({"QK_SM_CLUSTER": c, "QK_SM_KC": kc, "QK_SM_THREADS": t})
+    envs = [{}, {"QK_SM_POLICY": 1}, {"QK_SM_CLUSTER": 9, "QK_SM_POLICY": 1},
+            {"QK_SM_CLUSTER": 14, "QK_SM_KC": 15, "QK_SM_THREADS": 160, "QK_SM_POLICY": 1},
+            {"QK_SM_CLUSTER": 16, "QK_SM_POLICY": 1}, {"QK_SM_CLUSTER": 8, "QK_SM_POLICY": 1},
+            {"QK_SM_CLUSTER": 9, "QK_SM_KC": 16, "QK_SM_THREADS": 224}]
     for env in envs:
         try:
             ms, plan = time_plan(w, x, y, env)

@@ -178,3 +178,16 @@ def test_exact_kernel_close_to_reference():
     from oracle.oracle import EXACT
     y = _gpu_softmax(x, cols, 0.125, EXACT)
     assert max_rel(y, R.softmax_rows(x, cols, 0.125, EXACT, sum_mode=1)) <= 1e-5
+
+
+def test_interleaved_shapes_keep_launching():
+    """Planning one row length must not invalidate another's launch configuration
+    (regression: occupancy queries used to lower the smem attribute)."""
+    R = restatement()
+    shapes = (128256, 16384, 4096, 300000, 50000, 128256, 2048, 128256)
+    for cols in shapes:
+        rows = 2 if cols > 100000 else 8
+        x = (np.random.default_rng(cols).standard_normal(rows * cols) * 4).astype(np.float32)
+        y = _gpu_softmax(x, cols, 1.0, QUAKE2)
+        assert_bitexact(y, R.softmax_rows_ordered(x, cols, qk.softmax_plan(cols, True), 1.0,
+                                                  QUAKE2), f"cols={cols}")
