@@ -53,6 +53,7 @@ enum class SmVariant : int {
   kSmem = 2,        // CTA (or cluster of CTAs) per row, row staged in smem
   kGlobal3 = 3,     // CTA per row, three sweeps over global memory (huge rows)
   kPipe = 4,        // persistent cluster per row group, multi-stage TMA pipeline
+  kPipeLA = 5,      // kPipe with the cluster exchange awaited one row late
 };
 
 struct SmPlan {
@@ -82,6 +83,19 @@ SmPlan plan_softmax(size_t cols, bool aligned16, int device);
 
 // Launch softmax over `rows` rows of `cols` columns. `flags` (device, may be
 // null) receives bit 0 when a non-finite input was seen.
+// Per-kind launchers (softmax_k_*.cu) and the planner's occupancy probe.
+#define QK_SOFTMAX_LAUNCHER(name)                                                        \
+  cudaError_t launch_softmax_##name(const SmPlan& plan, const float* in, float* out,      \
+                                    size_t rows, size_t cols, const SmParams& p,         \
+                                    uint32_t* flags, cudaStream_t stream);
+QK_SOFTMAX_LAUNCHER(exact)
+QK_SOFTMAX_LAUNCHER(fast)
+QK_SOFTMAX_LAUNCHER(quake)
+QK_SOFTMAX_LAUNCHER(quake2)
+QK_SOFTMAX_LAUNCHER(quake2g)
+#undef QK_SOFTMAX_LAUNCHER
+int pipe_resident_probe(int variant, int cluster, int threads, size_t smem);
+
 cudaError_t launch_softmax(SmKernel k, const SmPlan& plan, const float* in, float* out,
                            size_t rows, size_t cols, const SmParams& p, uint32_t* flags,
                            cudaStream_t stream);

@@ -1,0 +1,20 @@
+// Row softmax instantiations for SmKernel::kQuake2 (see softmax_kernels.cuh).
+#include "softmax_kernels.cuh"
+
+namespace qk {
+
+cudaError_t launch_softmax_quake2(const SmPlan& plan, const float* in, float* out, size_t rows,
+                                  size_t cols, const SmParams& p, uint32_t* flags,
+                                  cudaStream_t stream) {
+  return launch_k<SmKernel::kQuake2>(plan, in, out, rows, cols, p, flags, stream);
+}
+
+// Clusters of the persistent pipelines resident at once for one launch shape
+// (the planner's occupancy probe; variant 4 = kPipe, 5 = kPipeLA).
+int pipe_resident_probe(int variant, int cluster, int threads, size_t smem) {
+  return variant == 5 ? resident_clusters(softmax_pipe_la<SmKernel::kQuake2, 8>, cluster, threads, smem)
+                      : resident_clusters(softmax_pipe<SmKernel::kQuake2, true, 16>, cluster, threads,
+                                          smem);
+}
+
+}  // namespace qk

@@ -16,7 +16,7 @@ from paper_2412_00408_b200.workloads import CONFIGS  # noqa: E402
 
 def time_plan(w, x, y, env, iters=10):
     for k in ("QK_SM_CLUSTER", "QK_SM_STAGES", "QK_SM_THREADS", "QK_SM_SMEM_KB", "QK_SM_KC",
-              "QK_SM_DELAY", "QK_SM_POLICY"):
+              "QK_SM_LA"):
         os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
     L = _lib.lib()
@@ -43,10 +43,7 @@ def main():
     x = w.device()
     y = torch.empty_like(x)
     ref = None
-    envs = [{}, {"QK_SM_POLICY": 1}, {"QK_SM_CLUSTER": 9, "QK_SM_POLICY": 1},
-            {"QK_SM_CLUSTER": 14, "QK_SM_KC": 15, "QK_SM_THREADS": 160, "QK_SM_POLICY": 1},
-            {"QK_SM_CLUSTER": 16, "QK_SM_POLICY": 1}, {"QK_SM_CLUSTER": 8, "QK_SM_POLICY": 1},
-            {"QK_SM_CLUSTER": 9, "QK_SM_KC": 16, "QK_SM_THREADS": 224}]
+    envs = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [{}]
     for env in envs:
         try:
             ms, plan = time_plan(w, x, y, env)
