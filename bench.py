@@ -273,6 +273,10 @@ def main():
 
     peak, peak_kind = hbm_peak()
     achieved = BYTES_PER_ELEM * n_local / (kern_ms * 1e-3) / 1e9
+    plan = qk.softmax_plan(w.cols, True)
+    kernel_name = {0: "softmax_warp_vec", 1: "softmax_warp_scalar", 2: "softmax_smem",
+                   3: "softmax_global3", 4: "softmax_pipe (TMA pipeline, cluster)",
+                   5: "softmax_pipe_la (lookahead TMA pipeline, cluster)"}[plan["variant"]]
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,
@@ -282,10 +286,10 @@ def main():
                    "temperature": w.temperature, "rows_per_gpu": my_rows,
                    "distribution": "N(0,4) seed 5 (torch CUDA Philox)",
                    "l2": "inputs (2.1 GB) larger than L2 (126 MB); no flush needed",
-                   "plan": qk.softmax_plan(w.cols, True)},
+                   "plan": plan},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "peak_kind": peak_kind, "kernel": "softmax_smem (cluster)",
+                     "peak_kind": peak_kind, "kernel": kernel_name,
                      "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n_local,
                      "avg_launch_us": kern_ms * 1e3},
         "e2e": {"value": e2e_value, "unit": "elements/s",

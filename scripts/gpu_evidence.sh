@@ -12,7 +12,7 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 CMD="python bench.py --steps 3 --warmup 3 --no-extras --e2e-steps 1"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:softmax_pipe -s 3 -c 1 -o gpurun_out/prof_softmax_pipe -f $CMD > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:softmax_pipe -s 3 -c 1 -o /tmp/prof_softmax_pipe -f $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu pipe exit $?" >> gpurun_out/ncu_full.log
 CMD2="python scripts/kernel_probe.py"
 timeout 300 $CMD2 > gpurun_out/kernel_probe.log 2>&1 && \
@@ -20,5 +20,7 @@ timeout 900 ncu --set full --clock-control none -k regex:"ew_vec_kernel|softmax_
 echo "ncu ew exit $?" >> gpurun_out/ncu_ew.log
 # summaries only (the full reports would exceed gpurun's 64 MiB copy-back)
 python scripts/ncu_summary.py /tmp/prof_ew.ncu-rep gpurun_out/ncu_ew_summary "elementwise + warp softmax" > /dev/null 2>&1
-python scripts/ncu_summary.py gpurun_out/prof_softmax_pipe.ncu-rep gpurun_out/ncu_pipe_summary "softmax_pipe cfg5" > /dev/null 2>&1
+python scripts/ncu_summary.py /tmp/prof_softmax_pipe.ncu-rep gpurun_out/ncu_pipe_summary "softmax_pipe cfg5" > /dev/null 2>&1
+python scripts/ncu_hot_sass.py /tmp/prof_softmax_pipe.ncu-rep gpurun_out/ncu_pipe_sass.txt 80 > /dev/null 2>&1
+ncu -i /tmp/prof_softmax_pipe.ncu-rep --page details --csv > gpurun_out/ncu_pipe_details.csv 2>&1
 du -sh gpurun_out
