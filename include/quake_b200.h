@@ -22,7 +22,9 @@
  *
  * KernelChoice values 0..2 match the reference enum (nonlin.hpp:32);
  * QK_EXPF and QK_FAST_EXP are GPU-only comparison kernels of identical
- * structure (CUDA expf / __expf in place of the QuAKE bit trick).
+ * structure (CUDA expf / __expf in place of the QuAKE bit trick);
+ * QK_QUAKE_UNFUSED / QK_QUAKE2_UNFUSED are the fusion-ablation variants of
+ * the reference bench (softmax and gelu only).
  */
 #ifndef QUAKE_B200_H_
 #define QUAKE_B200_H_
@@ -58,7 +60,13 @@ typedef enum {
   QK_QUAKE = 1,   /* KernelChoice::Quake  — first-order bit-trick exp */
   QK_QUAKE2 = 2,  /* KernelChoice::Quake2 — second-order mantissa refinement */
   QK_EXPF = 3,    /* comparison: QuAKE structure with CUDA expf */
-  QK_FAST_EXP = 4 /* comparison: QuAKE structure with __expf */
+  QK_FAST_EXP = 4,/* comparison: QuAKE structure with __expf */
+  /* fusion ablation (bench.cpp:137-166, 212-233; softmax and gelu only): the
+   * affine transform (t*(x - m), resp. fused_scale*x*(1/kappa + x*x)) is
+   * computed explicitly and fed to the plain natural / negated-natural
+   * QuAKE kernel instead of being folded into c0/c1. */
+  QK_QUAKE_UNFUSED = 5,
+  QK_QUAKE2_UNFUSED = 6
 } qk_kernel;
 
 /* kernels.hpp:39-46 AffineCoeffs */

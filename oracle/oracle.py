@@ -25,6 +25,8 @@ RESTATEMENT_SO = os.path.join(HERE, "liboracle.so")
 REFERENCE_SO = os.path.join(HERE, "_ref", "libquake_ref.so")
 
 EXACT, QUAKE, QUAKE2 = 0, 1, 2
+# unfused ablation variants of the bench passes (bench.cpp:137-166, 212-233)
+QUAKE_UNFUSED, QUAKE2_UNFUSED = 5, 6
 CONTINUITY = (np.float32(1.0) / np.float32(3.0), np.float32(0.0), np.float32(2.0) / np.float32(3.0))
 MINIMAX = (np.float32(0.33), np.float32(-0.017), np.float32(0.68))
 
@@ -231,6 +233,10 @@ class Reference:
             getattr(L, name).argtypes = [c_double]
             getattr(L, name).restype = c_double
         L.ref_exact_softmax.argtypes = [_fp, c_size_t, c_double, _dp]
+        L.ref_bench_inputs.argtypes = [c_int, c_size_t, c_uint64, _fp]
+        L.ref_bench_inputs.restype = None
+        L.ref_fusion_ablation.argtypes = [c_int, c_int, c_size_t, c_size_t, c_size_t, c_float,
+                                          c_uint64, _dp, _dp, _dp]
 
     def _check(self, st):
         if st != 0:
@@ -331,6 +337,22 @@ class Reference:
         out = np.empty(v.size, dtype=np.float64)
         self._check(self.lib.ref_exact_softmax(_ptr(v), v.size, t, _ptr(out, _dp)))
         return out
+
+    # --- bench.cpp: the fusion ablation's inputs and checksums ---
+    WORKLOADS = {"softmax_matrix": 0, "gelu_vector": 1, "exp_vector": 2, "logistic_vector": 3}
+
+    def bench_inputs(self, workload: str, count: int, seed: int = 42) -> np.ndarray:
+        out = np.empty(count, dtype=np.float32)
+        self.lib.ref_bench_inputs(self.WORKLOADS[workload], count, seed, _ptr(out))
+        return out
+
+    def fusion_ablation(self, workload: str, kernel: int, rows=0, cols=0, n=0,
+                        temperature=1.0, seed=42):
+        """(fused checksum, unfused checksum, max rel divergence), bench.cpp:425-513."""
+        f, u, d = c_double(), c_double(), c_double()
+        self._check(self.lib.ref_fusion_ablation(self.WORKLOADS[workload], kernel, rows, cols, n,
+                                                 temperature, seed, f, u, d))
+        return f.value, u.value, d.value
 
 
 def restatement() -> Restatement:

@@ -129,9 +129,17 @@ void or_quake2_buffer(const float* xs, float* out, size_t n, float c0, float c1,
   }
 }
 
-/* nonlin.hpp:39-41 resolve_centering_bias. */
+static int is_unfused(int kernel) {
+  return kernel == OR_QUAKE_UNFUSED || kernel == OR_QUAKE2_UNFUSED;
+}
+/* the exponential body an (un)fused kernel id uses: OR_QUAKE or OR_QUAKE2 */
+static int body_of(int kernel) {
+  return kernel == OR_QUAKE_UNFUSED ? OR_QUAKE : kernel == OR_QUAKE2_UNFUSED ? OR_QUAKE2 : kernel;
+}
+
+/* nonlin.hpp:39-41 resolve_centering_bias (unfused ids resolve as their body). */
 static int resolve_bias(int kernel, int requested) {
-  return requested < 0 ? (kernel == OR_QUAKE) : (requested != 0);
+  return requested < 0 ? (body_of(kernel) == OR_QUAKE) : (requested != 0);
 }
 
 void or_logistic_buffer(const float* xs, float* out, size_t n, int kernel, int bias) {
@@ -174,8 +182,23 @@ void or_gelu_buffer(const float* xs, float* out, size_t n, int kernel, int bias)
     }
     return;
   }
-  /* nonlin.cpp:248-264 gelu_exp_kernel: slope -log2e * fused_scale. */
   float c0, c1, lo, hi;
+  if (is_unfused(kernel)) {
+    /* bench.cpp:212-233: w = fused_scale*x*(inverse_kappa + x*x) computed
+     * explicitly, fed to the e^-x kernel (negated natural coefficients). */
+    or_coeffs_for((float)(-kLog2e), 0.0f, resolve_bias(kernel, bias), &c0, &c1);
+    or_clamp_for(c0, c1, &lo, &hi);
+    for (size_t i = 0; i < n; ++i) {
+      const float x = xs[i];
+      const float w = fs * x * (ik + x * x);
+      const float s = saturate(w, lo, hi);
+      const float e = body_of(kernel) == OR_QUAKE ? quake_body(s, c0, c1)
+                                                  : quake2_body(s, c0, c1, 0, 0.f, 0.f, 0.f);
+      out[i] = x / (1.0f + e);
+    }
+    return;
+  }
+  /* nonlin.cpp:248-264 gelu_exp_kernel: slope -log2e * fused_scale. */
   or_coeffs_for((float)(-kLog2e * (double)fs), 0.0f, resolve_bias(kernel, bias), &c0, &c1);
   or_clamp_for(c0, c1, &lo, &hi);
   for (size_t i = 0; i < n; ++i) {
@@ -209,6 +232,50 @@ static int row_max_checked(const float* v, size_t n, float* m_out) {
   return OR_OK;
 }
 
+/* Per-row exponential of the QuAKE softmax kernels. Fused (nonlin.cpp:
+ * 85-116): c0/c1 carry temperature and row max, inputs clamped below at
+ * v_min. Unfused (bench.cpp:137-166): tmp = t*(x - m) explicitly, saturated
+ * to the natural-exp clamp range, plain natural-exp body. */
+typedef struct {
+  int body, general, unfused;
+  float c0, c1, v_min, a0, a1, a2;
+  float m, t, lo, hi;
+} row_exp_ctx;
+
+static row_exp_ctx row_exp_setup(float m, float t, int kernel, int bias_req, float a0, float a1,
+                                 float a2) {
+  row_exp_ctx c;
+  c.body = body_of(kernel);
+  c.unfused = is_unfused(kernel);
+  c.general = c.unfused ? 0 : !is_continuity(a0, a1, a2);
+  c.a0 = a0;
+  c.a1 = a1;
+  c.a2 = a2;
+  c.m = m;
+  c.t = t;
+  if (c.unfused) {
+    or_coeffs_for((float)kLog2e, 0.0f, resolve_bias(kernel, bias_req), &c.c0, &c.c1);
+    or_clamp_for(c.c0, c.c1, &c.lo, &c.hi);
+    c.v_min = 0.0f;
+  } else {
+    or_softmax_row_scalars(m, t, resolve_bias(kernel, bias_req), &c.c0, &c.c1, &c.v_min);
+    c.lo = c.hi = 0.0f;
+  }
+  return c;
+}
+
+static float row_exp_elem(const row_exp_ctx* c, float x) {
+  float u;
+  if (c->unfused) {
+    const float tmp = c->t * (x - c->m);
+    u = saturate(tmp, c->lo, c->hi);
+  } else {
+    u = x > c->v_min ? x : c->v_min;
+  }
+  return c->body == OR_QUAKE ? quake_body(u, c->c0, c->c1)
+                             : quake2_body(u, c->c0, c->c1, c->general, c->a0, c->a1, c->a2);
+}
+
 /* nonlin.cpp:59-116 softmax_row_with + softmax_row_unchecked. */
 static void softmax_row_unchecked(const float* v, size_t n, float m, float t,
                                   int bias_req, float a0, float a1, float a2,
@@ -226,15 +293,11 @@ static void softmax_row_unchecked(const float* v, size_t n, float m, float t,
     for (size_t i = 0; i < n; ++i) out[i] /= sum;
     return;
   }
-  float c0, c1, v_min;
-  or_softmax_row_scalars(m, t, resolve_bias(kernel, bias_req), &c0, &c1, &v_min);
-  const int general = !is_continuity(a0, a1, a2);
+  const row_exp_ctx ctx = row_exp_setup(m, t, kernel, bias_req, a0, a1, a2);
   float fsum = 0.0f;
   double dsum = 0.0;
   for (size_t i = 0; i < n; ++i) {
-    const float u = v[i] > v_min ? v[i] : v_min;
-    const float y = kernel == OR_QUAKE ? quake_body(u, c0, c1)
-                                       : quake2_body(u, c0, c1, general, a0, a1, a2);
+    const float y = row_exp_elem(&ctx, v[i]);
     out[i] = y;
     fsum += y;
     dsum += (double)y;
@@ -304,21 +367,16 @@ int or_softmax_rows_ordered(const float* mat, size_t n, size_t cols, float tempe
     const int st = row_max_checked(mat + r * cols, cols, &m);
     if (st != OR_OK) return st;
   }
-  const int general = !is_continuity(a0, a1, a2);
   const long long nchunks = (long long)(cols / (size_t)width);
   if (slice <= 0) { slice = nchunks; cluster = 1; balanced = 0; }
   float part[1024];
   for (size_t r = 0; r < rows; ++r) {
     const float* v = mat + r * cols;
     float* y = out + r * cols;
-    float m = 0.0f, c0, c1, v_min;
+    float m = 0.0f;
     row_max_checked(v, cols, &m);
-    or_softmax_row_scalars(m, temperature, resolve_bias(kernel, bias_req), &c0, &c1, &v_min);
-    for (size_t i = 0; i < cols; ++i) {
-      const float u = v[i] > v_min ? v[i] : v_min;
-      y[i] = kernel == OR_QUAKE ? quake_body(u, c0, c1)
-                                : quake2_body(u, c0, c1, general, a0, a1, a2);
-    }
+    const row_exp_ctx ctx = row_exp_setup(m, temperature, kernel, bias_req, a0, a1, a2);
+    for (size_t i = 0; i < cols; ++i) y[i] = row_exp_elem(&ctx, v[i]);
     float S = 0.0f;
     const long long q = nchunks / cluster, rem = nchunks % cluster;
     for (int c = 0; c < cluster; ++c) {

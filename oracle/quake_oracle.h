@@ -27,6 +27,11 @@ extern "C" {
 #endif
 
 enum { OR_EXACT = 0, OR_QUAKE = 1, OR_QUAKE2 = 2 };
+/* Unfused ablation variants of the bench passes (bench.cpp:137-166 softmax,
+ * :212-233 GELU): the affine transform is computed explicitly and fed to
+ * the plain natural / negated-natural exponential kernel. Softmax and GELU
+ * only; the centering bias resolves as for the base kernel. */
+enum { OR_QUAKE_UNFUSED = 5, OR_QUAKE2_UNFUSED = 6 };
 
 /* Status codes (match include/quake_b200.h's qk_status for the shared cases). */
 enum {

@@ -10,12 +10,16 @@
 //   nonlin.hpp:70-97    softmax_row(s), logistic_buffer, gelu_buffer
 //   kernels.hpp:47-51, 86-88   coeffs_for / clamp_for / default_clamp
 //   oracle.hpp:28-42    exact_* ground truth
+//   bench.hpp:74-83     fusion_ablation (checksums pin the unfused restatement)
 #include <cstring>
 #include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
 
+#include <random>
+
+#include "quake/bench.hpp"
 #include "quake/kernels.hpp"
 #include "quake/nonlin.hpp"
 #include "quake/oracle.hpp"
@@ -182,6 +186,39 @@ double ref_exact_gelu_tanh(double x) { return quake::oracle::exact_gelu_tanh(x);
 int ref_exact_softmax(const float* v, size_t n, double t, double* out) {
   return guarded([&] {
     quake::oracle::exact_softmax(std::span<const float>(v, n), t, std::span<double>(out, n));
+  });
+}
+
+// The reference bench's input generator (bench.cpp:48-60 input_range,
+// :341-348 fill_inputs): mt19937_64(seed), uniform float in the workload's
+// range; workload 0 softmax_matrix, 1 gelu_vector, 2 exp_vector, 3 logistic_vector.
+void ref_bench_inputs(int workload, size_t count, uint64_t seed, float* out) {
+  static const float lo[] = {-8.0f, -6.0f, -20.0f, -12.0f};
+  static const float hi[] = {8.0f, 6.0f, 20.0f, 12.0f};
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<float> dist(lo[workload], hi[workload]);
+  for (size_t i = 0; i < count; ++i) out[i] = dist(rng);
+}
+
+// bench.cpp:425-513 fusion_ablation: the checksums (sum of outputs in
+// double) of the fused and unfused passes and their max relative divergence.
+int ref_fusion_ablation(int workload, int kernel, size_t rows, size_t cols, size_t n,
+                        float temperature, uint64_t seed, double* fused_checksum,
+                        double* unfused_checksum, double* divergence) {
+  return guarded([&] {
+    quake::bench::BenchConfig cfg;
+    cfg.workload = workload == 0 ? quake::bench::Workload::SoftmaxMatrix
+                                 : quake::bench::Workload::GeluVector;
+    cfg.rows = rows;
+    cfg.cols = cols;
+    cfg.n = n;
+    cfg.kernel = kernel_of(kernel);
+    cfg.temperature = temperature;
+    cfg.seed = seed;
+    const quake::bench::AblationReport r = quake::bench::fusion_ablation(cfg);
+    *fused_checksum = r.fused.checksum;
+    *unfused_checksum = r.unfused.checksum;
+    *divergence = r.max_rel_divergence;
   });
 }
 

@@ -69,6 +69,17 @@ __device__ __forceinline__ float apply(float x, const EwParams& p) {
     // SSE's divss returns x quieted (payload kept).
     const float y = __fdiv_rn(x, __fadd_rn(1.0f, e));
     return y != y ? x86_quiet(x) : y;
+  } else if constexpr (OP == EwOp::kGeluQuakeUnfused || OP == EwOp::kGeluQuake2Unfused) {
+    // bench.cpp:212-233 (ablation): w = fused_scale*x*(inverse_kappa + x*x)
+    // computed explicitly (k1 = fused_scale), then x / (1 + e^-w) with the
+    // negated natural-exp coefficients in c0/c1.
+    const float w = __fmul_rn(__fmul_rn(p.k1, x), __fadd_rn(p.k0, __fmul_rn(x, x)));
+    const float s = saturate_fast(w, p.lo, p.hi);
+    const float e = OP == EwOp::kGeluQuakeUnfused
+                        ? quake_body(s, p.c0, p.c1)
+                        : quake2_body<false>(s, p.c0, p.c1, 0.f, 0.f, 0.f);
+    const float y = __fdiv_rn(x, __fadd_rn(1.0f, e));
+    return y != y ? x86_quiet(x) : y;
   } else if constexpr (OP == EwOp::kGeluTanh) {
     // nonlin.cpp:302-304: 0.5f*x*(1 + tanh(r2pi*(x + kappa*x*x*x)))
     const float cube = __fmul_rn(__fmul_rn(__fmul_rn(p.k1, x), x), x);
@@ -270,6 +281,10 @@ cudaError_t launch_elementwise(EwOp op, const float* in, float* out, size_t n, c
     case EwOp::kGeluTanh: return launch_op<EwOp::kGeluTanh, false>(in, out, n, p, sm_count, stream);
     case EwOp::kGeluExpf: return launch_op<EwOp::kGeluExpf, false>(in, out, n, p, sm_count, stream);
     case EwOp::kGeluFast: return launch_op<EwOp::kGeluFast, false>(in, out, n, p, sm_count, stream);
+    case EwOp::kGeluQuakeUnfused:
+      return launch_op<EwOp::kGeluQuakeUnfused, false>(in, out, n, p, sm_count, stream);
+    case EwOp::kGeluQuake2Unfused:
+      return launch_op<EwOp::kGeluQuake2Unfused, false>(in, out, n, p, sm_count, stream);
   }
   return cudaErrorInvalidValue;
 }

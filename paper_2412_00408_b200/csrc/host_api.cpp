@@ -86,8 +86,8 @@ bool is_continuity(const qk_quad_coeffs& a) {
 }
 
 bool resolve_bias(qk_kernel k, int32_t requested) {
-  // nonlin.hpp:39-41
-  return requested < 0 ? (k == QK_QUAKE) : (requested != 0);
+  // nonlin.hpp:39-41 (the unfused ablation kernels resolve as their QuAKE body)
+  return requested < 0 ? (k == QK_QUAKE || k == QK_QUAKE_UNFUSED) : (requested != 0);
 }
 
 qk_gelu_constants gelu_defaults() {
@@ -292,6 +292,18 @@ qk_status resolve_ew(Family f, qk_kernel k, int32_t bias_req, const qk_affine_co
         p.lo = rc.lo;
         p.hi = rc.hi;
         out->op = k == QK_QUAKE ? qk::EwOp::kGeluQuake : qk::EwOp::kGeluQuake2;
+      } else if (k == QK_QUAKE_UNFUSED || k == QK_QUAKE2_UNFUSED) {
+        // bench.cpp:212-233: explicit fused_scale*x*(ik + x*x) into e^-w
+        const qk_affine_coeffs ce = make_coeffs(static_cast<float>(-kLog2e), 0.0f,
+                                                resolve_bias(k, bias_req));
+        const qk_clamp_range rc = solve_clamp(ce.c0, ce.c1);
+        p.c0 = ce.c0;
+        p.c1 = ce.c1;
+        p.lo = rc.lo;
+        p.hi = rc.hi;
+        p.k1 = g.fused_scale;
+        out->op = k == QK_QUAKE_UNFUSED ? qk::EwOp::kGeluQuakeUnfused
+                                        : qk::EwOp::kGeluQuake2Unfused;
       } else {
         return fail(QK_ERR_BAD_ARGUMENT, "gelu_buffer: unknown kernel choice");
       }
@@ -319,6 +331,20 @@ qk_status resolve_sm(const qk_softmax_params* prm, qk_kernel k, qk::SmKernel* sk
     case QK_EXPF: *sk = qk::SmKernel::kExpf; break;
     case QK_FAST_EXP: *sk = qk::SmKernel::kFast; break;
     case QK_QUAKE: *sk = qk::SmKernel::kQuake; break;
+    case QK_QUAKE_UNFUSED:
+    case QK_QUAKE2_UNFUSED: {
+      // bench.cpp:137-166: natural-exp coefficients and clamp, per-kernel bias
+      const qk_affine_coeffs ce = make_coeffs(static_cast<float>(kLog2e), 0.0f,
+                                              resolve_bias(k, prm->centering_bias));
+      const qk_clamp_range rc = solve_clamp(ce.c0, ce.c1);
+      p.nat_c0 = ce.c0;
+      p.nat_c1 = ce.c1;
+      p.nat_lo = rc.lo;
+      p.nat_hi = rc.hi;
+      p.unfused = 1;
+      *sk = k == QK_QUAKE_UNFUSED ? qk::SmKernel::kQuakeUnfused : qk::SmKernel::kQuake2Unfused;
+      break;
+    }
     case QK_QUAKE2:
       if (is_continuity(prm->quad)) {
         *sk = qk::SmKernel::kQuake2;
@@ -650,6 +676,8 @@ const char* qk_kernel_name(qk_kernel k) {
     case QK_QUAKE2: return "quake2";
     case QK_EXPF: return "expf";
     case QK_FAST_EXP: return "fast_expf";
+    case QK_QUAKE_UNFUSED: return "quake_unfused";
+    case QK_QUAKE2_UNFUSED: return "quake2_unfused";
   }
   return "unknown";
 }

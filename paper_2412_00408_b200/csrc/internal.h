@@ -25,6 +25,8 @@ enum class EwOp : int {
   kGeluTanh = 11,     // nonlin.cpp:298-306 (Exact, tanh form)
   kGeluExpf = 12,     // comparison: sigmoid form with expf
   kGeluFast = 13,     // comparison: sigmoid form with __expf
+  kGeluQuakeUnfused = 14,  // ablation: bench.cpp:212-233, w = fs*x*(ik + x*x) into e^-w
+  kGeluQuake2Unfused = 15,
 };
 
 struct EwParams {
@@ -43,7 +45,10 @@ cudaError_t launch_elementwise(EwOp op, const float* in, float* out, size_t n,
 // ---- row softmax ----
 
 enum class SmKernel : int { kExact = 0, kQuake = 1, kQuake2 = 2, kQuake2General = 3,
-                            kExpf = 4, kFast = 5 };
+                            kExpf = 4, kFast = 5,
+                            // ablation (bench.cpp:137-166): t*(x - m) computed
+                            // explicitly, natural-exp QuAKE on the saturated value
+                            kQuakeUnfused = 6, kQuake2Unfused = 7 };
 
 // Reduction geometry of one launch (also reported through qk_softmax_plan so
 // the tests can restate the exact summation order).
@@ -77,6 +82,8 @@ struct SmParams {
   double vmin_off;  // 126 * ln2 / t                 nonlin.cpp:92-93
   float a0, a1, a2; // quad (kQuake2General)
   int general_quad; // 1: y_m may leave [1, 2]; rows use SSE-exact semantics
+  float nat_c0, nat_c1, nat_lo, nat_hi;  // unfused kinds: natural-exp coefficients / clamp
+  int unfused;      // 1: kQuakeUnfused / kQuake2Unfused
 };
 
 SmPlan plan_softmax(size_t cols, bool aligned16, int device);
@@ -93,6 +100,8 @@ QK_SOFTMAX_LAUNCHER(fast)
 QK_SOFTMAX_LAUNCHER(quake)
 QK_SOFTMAX_LAUNCHER(quake2)
 QK_SOFTMAX_LAUNCHER(quake2g)
+QK_SOFTMAX_LAUNCHER(quake_unfused)
+QK_SOFTMAX_LAUNCHER(quake2_unfused)
 #undef QK_SOFTMAX_LAUNCHER
 int pipe_resident_probe(int variant, int cluster, int threads, size_t smem);
 

@@ -59,6 +59,8 @@ class KernelChoice(enum.IntEnum):
     Quake2 = 2
     Expf = 3      # QuAKE structure with CUDA expf
     FastExp = 4   # QuAKE structure with __expf
+    QuakeUnfused = 5   # fusion ablation (bench.cpp:137-166, 212-233): softmax / gelu only
+    Quake2Unfused = 6
 
 
 def kernel_name(k: KernelChoice) -> str:

@@ -115,6 +115,8 @@ def test_validation_errors_match_reference_messages():
         (lambda: qk.softmax_row(x, qk.SoftmaxParams(), K.Exact, out=np.zeros(3, np.float32)),
          "softmax_row: output size mismatch"),
         (lambda: qk.coeffs_for(0.0, 1.0), "coeffs_for: input scale p must be non-zero"),
+        # the fusion-ablation kernels exist for softmax and gelu only
+        (lambda: qk.logistic_buffer(x, K.QuakeUnfused), "logistic_buffer: unknown kernel choice"),
         (lambda: qk.default_clamp(0.0, 0.0), "default_clamp: input scale p must be non-zero"),
     ]
     for fn, msg in cases:
@@ -165,3 +167,16 @@ def test_cuda_calls_fail_loudly_without_gpu():
     K = qk.KernelChoice
     with pytest.raises(qk.QuakeCudaError):
         qk.logistic_buffer(np.ones(16, np.float32), K.Quake)
+
+
+def test_kernel_names_and_unfused_bias_resolution():
+    K = qk.KernelChoice
+    names = {K.Exact: "exact", K.Quake: "quake", K.Quake2: "quake2", K.Expf: "expf",
+             K.FastExp: "fast_expf", K.QuakeUnfused: "quake_unfused",
+             K.Quake2Unfused: "quake2_unfused"}
+    for k, name in names.items():
+        assert qk.kernel_name(k) == name
+    # the unfused ablation kernels resolve the centering bias as their QuAKE body
+    assert qk.resolve_centering_bias(K.QuakeUnfused, None) is True
+    assert qk.resolve_centering_bias(K.Quake2Unfused, None) is False
+    assert qk.resolve_centering_bias(K.Quake2Unfused, True) is True

@@ -189,3 +189,38 @@ def test_ordered_restatement_is_a_reordering_only():
     a = R.softmax_rows_ordered(m, 128256, cplan, 1.0, QUAKE2)
     b = R.softmax_rows(m, 128256, 1.0, QUAKE2, sum_mode=1)
     assert np.max(np.abs(a.astype(np.float64) - b) / b) <= 2e-6
+
+
+@pytest.mark.skipif(reference() is None, reason="reference not compiled here")
+def test_unfused_restatement_pinned_to_reference_fusion_ablation():
+    """The ablation's unfused passes (bench.cpp:137-166, 212-233), restated as kernel ids
+    QUAKE_UNFUSED / QUAKE2_UNFUSED, reproduce the reference's own fusion_ablation
+    checksums exactly (sum of outputs in fp64, bench.cpp:309-313) — and so do the fused
+    passes through the regular softmax / gelu restatement — on the reference's inputs."""
+    from oracle.oracle import QUAKE2_UNFUSED, QUAKE_UNFUSED
+    R, F = restatement(), reference()
+
+    def checksum(y):
+        s = 0.0
+        for v in np.asarray(y, np.float64):
+            s += v
+        return s
+
+    for kern, unf in ((QUAKE, QUAKE_UNFUSED), (QUAKE2, QUAKE2_UNFUSED)):
+        for rows, cols, t, seed in ((37, 1000, 0.7, 42), (5, 4096, 1.0, 7), (64, 33, 0.125, 3)):
+            x = F.bench_inputs("softmax_matrix", rows * cols, seed)
+            fc, uc, div = F.fusion_ablation("softmax_matrix", kern, rows, cols, 0, t, seed)
+            yf = R.softmax_rows(x, cols, t, kern, sum_mode=0)
+            yu = R.softmax_rows(x, cols, t, unf, sum_mode=0)
+            assert checksum(yf) == fc and checksum(yu) == uc, (kern, rows, cols, t)
+            rel = np.abs(yf.astype(np.float64) - yu) / np.maximum(np.abs(yf), np.abs(yu))
+            assert rel.max() == div
+        for n, seed in ((100003, 42), (4099, 9)):
+            x = F.bench_inputs("gelu_vector", n, seed)
+            fc, uc, div = F.fusion_ablation("gelu_vector", kern, 0, 0, n, 1.0, seed)
+            yf, yu = R.gelu_buffer(x, kern), R.gelu_buffer(x, unf)
+            assert checksum(yf) == fc and checksum(yu) == uc, (kern, n)
+            a, b = yf.astype(np.float64), yu.astype(np.float64)
+            den = np.maximum(np.abs(a), np.abs(b))
+            rel = np.where(den > 0, np.abs(a - b) / np.where(den > 0, den, 1), 0)
+            assert rel.max() == div
