@@ -87,4 +87,11 @@ CFG5 = Workload("cfg5_softmax_vocab", "softmax", (4096, 128256), "normal", 0.0, 
                 temperature=1.0, kernels=("quake2",),
                 description="row softmax over LM vocab logits 4096x128256, QuAKE2")
 
+# Not a bench line: the paper's Table III softmax size (§V-A2,
+# 16384x16384, bench.cpp:48-60 input range), used for plan tuning / ablation.
+PAPER_SOFTMAX = Workload("paper_softmax_16k", "softmax", (16384, 16384), "uniform", -8.0, 8.0,
+                         42, temperature=1.0, kernels=("quake", "quake2"),
+                         description="Table III softmax matrix 16384x16384, U(-8, 8)")
+
 CONFIGS = {w.name: w for w in (CFG1, CFG2, CFG3, CFG4, CFG5)}
+TUNING = {PAPER_SOFTMAX.name: PAPER_SOFTMAX}

@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 import paper_2412_00408_b200 as qk  # noqa: E402
 from paper_2412_00408_b200 import _lib  # noqa: E402
-from paper_2412_00408_b200.workloads import CONFIGS  # noqa: E402
+from paper_2412_00408_b200.workloads import CONFIGS, TUNING  # noqa: E402
 
 
 def time_plan(w, x, y, env, iters=10):
@@ -39,7 +39,12 @@ def time_plan(w, x, y, env, iters=10):
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg5_softmax_vocab"
-    w = CONFIGS[name]
+    if name.startswith("shape:"):  # shape:ROWSxCOLS, N(0, 4)
+        from paper_2412_00408_b200.workloads import Workload
+        r, c = (int(v) for v in name[6:].split("x"))
+        w = Workload(name, "softmax", (r, c), "normal", 0.0, 4.0, 1)
+    else:
+        w = {**CONFIGS, **TUNING}[name]
     x = w.device()
     y = torch.empty_like(x)
     ref = None
