@@ -237,6 +237,16 @@ class Reference:
         L.ref_bench_inputs.restype = None
         L.ref_fusion_ablation.argtypes = [c_int, c_int, c_size_t, c_size_t, c_size_t, c_float,
                                           c_uint64, _dp, _dp, _dp]
+        _u64p = POINTER(c_uint64)
+        L.ref_sweep_error.argtypes = [c_int, c_int, c_int, c_float, c_float, c_float, c_float,
+                                      c_float, c_uint64, c_uint, _u64p, _dp, _dp, _fp]
+        L.ref_quad_max_rel_err.argtypes = [c_double, c_double, c_double, c_size_t]
+        L.ref_quad_max_rel_err.restype = c_double
+        L.ref_grid_search_quad.argtypes = [_dp, _fp, _dp, _u64p]
+        L.ref_continuity_probe.argtypes = [c_int, c_int, c_int, c_float, c_float, c_float, c_int,
+                                           c_int, _dp, _fp]
+        L.ref_bias_reoptimize.argtypes = [c_int, c_int, c_int, c_float, c_float, c_float,
+                                          c_double, c_double, _fp, _dp, POINTER(c_int)]
 
     def _check(self, st):
         if st != 0:
@@ -353,6 +363,37 @@ class Reference:
         self._check(self.lib.ref_fusion_ablation(self.WORKLOADS[workload], kernel, rows, cols, n,
                                                  temperature, seed, f, u, d))
         return f.value, u.value, d.value
+
+    # --- lab.cpp: the accuracy lab (pins the GPU lab) ---
+    def sweep_error(self, kind, natural=True, bias=True, quad=CONTINUITY, lo=-80.0, hi=80.0,
+                    uniform_samples=1 << 22, period_stride=1):
+        """(samples, max_rel_err, mean_rel_err, argmax_input), lab.cpp:150-200."""
+        n, mx, mean, arg = c_uint64(), c_double(), c_double(), c_float()
+        self._check(self.lib.ref_sweep_error(kind, int(natural), int(bias), *quad, lo, hi,
+                                             uniform_samples, period_stride, n, mx, mean, arg))
+        return n.value, mx.value, mean.value, np.float32(arg.value)
+
+    def quad_max_rel_err(self, a0, a1, a2, intervals=1 << 16):
+        return self.lib.ref_quad_max_rel_err(a0, a1, a2, intervals)
+
+    def grid_search_quad(self, axes=(0.30, 0.36, 0.001, -0.05, 0.02, 0.001, 0.64, 0.72, 0.001)):
+        ax = np.asarray(axes, np.float64)
+        best = np.zeros(3, np.float32)
+        err, pts = c_double(), c_uint64()
+        self._check(self.lib.ref_grid_search_quad(_ptr(ax, _dp), _ptr(best), err, pts))
+        return tuple(best), err.value, pts.value
+
+    def continuity_probe(self, kind, natural, bias, k_lo, k_hi, quad=CONTINUITY):
+        w, at = c_double(), c_float()
+        self._check(self.lib.ref_continuity_probe(kind, int(natural), int(bias), *quad, k_lo, k_hi,
+                                                  w, at))
+        return w.value, np.float32(at.value)
+
+    def bias_reoptimize(self, kind, natural=True, bias=True, quad=CONTINUITY, lo=0.0, hi=0.1):
+        b, err, near = c_float(), c_double(), c_int()
+        self._check(self.lib.ref_bias_reoptimize(kind, int(natural), int(bias), *quad, lo, hi, b,
+                                                 err, near))
+        return np.float32(b.value), err.value, bool(near.value)
 
 
 def restatement() -> Restatement:

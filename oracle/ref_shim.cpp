@@ -11,6 +11,8 @@
 //   kernels.hpp:47-51, 86-88   coeffs_for / clamp_for / default_clamp
 //   oracle.hpp:28-42    exact_* ground truth
 //   bench.hpp:74-83     fusion_ablation (checksums pin the unfused restatement)
+//   lab.hpp:70-125      sweep_error, quad_max_rel_err, grid_search_quad,
+//                       continuity_probe, bias_reoptimize (pin the GPU lab)
 #include <cstring>
 #include <optional>
 #include <span>
@@ -21,6 +23,7 @@
 
 #include "quake/bench.hpp"
 #include "quake/kernels.hpp"
+#include "quake/lab.hpp"
 #include "quake/nonlin.hpp"
 #include "quake/oracle.hpp"
 #include "quake/parallel.hpp"
@@ -219,6 +222,73 @@ int ref_fusion_ablation(int workload, int kernel, size_t rows, size_t cols, size
     *fused_checksum = r.fused.checksum;
     *unfused_checksum = r.unfused.checksum;
     *divergence = r.max_rel_divergence;
+  });
+}
+
+namespace {
+quake::lab::ExpConfig exp_config(int kind, int natural, int bias, float a0, float a1, float a2) {
+  quake::lab::ExpConfig c;
+  c.kind = kernel_of(kind);
+  c.natural_base = natural != 0;
+  c.centering_bias = bias != 0;
+  c.quad = quake::QuadCoeffs{a0, a1, a2};
+  return c;
+}
+}  // namespace
+
+int ref_sweep_error(int kind, int natural, int bias, float a0, float a1, float a2, float lo,
+                    float hi, uint64_t uniform_samples, uint32_t period_stride,
+                    uint64_t* samples, double* max_rel, double* mean_rel, float* argmax) {
+  return guarded([&] {
+    quake::lab::SweepSpec spec{lo, hi, uniform_samples, period_stride};
+    const quake::lab::ErrorReport r =
+        quake::lab::sweep_error(exp_config(kind, natural, bias, a0, a1, a2), spec);
+    *samples = r.samples;
+    *max_rel = r.max_rel_err;
+    *mean_rel = r.mean_rel_err;
+    *argmax = r.argmax_input;
+  });
+}
+
+double ref_quad_max_rel_err(double a0, double a1, double a2, size_t intervals) {
+  return quake::lab::quad_max_rel_err(a0, a1, a2, intervals);
+}
+
+int ref_grid_search_quad(const double* axes /* 9: lo, hi, step x3 */, float* best,
+                         double* best_err, uint64_t* points) {
+  return guarded([&] {
+    quake::lab::GridSpec g;
+    g.a0 = {axes[0], axes[1], axes[2]};
+    g.a1 = {axes[3], axes[4], axes[5]};
+    g.a2 = {axes[6], axes[7], axes[8]};
+    const quake::lab::GridSearchResult r = quake::lab::grid_search_quad(g);
+    best[0] = r.best.a0;
+    best[1] = r.best.a1;
+    best[2] = r.best.a2;
+    *best_err = r.best_max_rel_err;
+    *points = r.points_searched;
+  });
+}
+
+int ref_continuity_probe(int kind, int natural, int bias, float a0, float a1, float a2,
+                         int k_lo, int k_hi, double* worst, float* at) {
+  return guarded([&] {
+    const quake::lab::ContinuityReport r = quake::lab::continuity_probe(
+        exp_config(kind, natural, bias, a0, a1, a2), k_lo, k_hi);
+    *worst = r.worst_jump;
+    *at = r.at;
+  });
+}
+
+int ref_bias_reoptimize(int kind, int natural, int bias, float a0, float a1, float a2,
+                        double beta_lo, double beta_hi, float* beta, double* max_rel,
+                        int* near) {
+  return guarded([&] {
+    const quake::lab::BiasSearchResult r = quake::lab::bias_reoptimize(
+        exp_config(kind, natural, bias, a0, a1, a2), beta_lo, beta_hi);
+    *beta = r.beta;
+    *max_rel = r.max_rel_err;
+    *near = r.near_reference_bias ? 1 : 0;
   });
 }
 

@@ -1,4 +1,5 @@
-"""ctypes binding of ``libquake_b200.so`` (the C-ABI in include/quake_b200.h).
+"""ctypes binding of ``libquake_b200.so`` (the C-ABI in include/quake_b200.h and
+include/quake_b200_lab.h).
 
 Loading fails loudly: there is no CPU fallback anywhere in this package.
 """
@@ -6,8 +7,8 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import (POINTER, Structure, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t,
-                    c_uint32, c_void_p)
+from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int, c_int32, c_int64,
+                    c_size_t, c_uint32, c_uint64, c_void_p)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "libquake_b200.so")
@@ -53,6 +54,52 @@ class SoftmaxPlanC(Structure):
                 ("cluster", c_int32), ("slice", c_int64), ("threads", c_int32),
                 ("vpt", c_int32), ("smem", c_int64), ("stages", c_int32),
                 ("balanced", c_int32), ("resident", c_int32)]
+
+
+# ---- include/quake_b200_lab.h ----
+class ExpConfigC(Structure):
+    _fields_ = [("kind", c_int), ("natural_base", c_int32), ("centering_bias", c_int32),
+                ("quad", QuadCoeffsC)]
+
+
+class SweepSpecC(Structure):
+    _fields_ = [("lo", c_float), ("hi", c_float), ("uniform_samples", c_uint64),
+                ("period_stride", c_uint32)]
+
+
+class ErrorReportC(Structure):
+    _fields_ = [("lo", c_float), ("hi", c_float), ("samples", c_uint64),
+                ("max_rel_err", c_double), ("mean_rel_err", c_double),
+                ("argmax_input", c_float)]
+
+
+class ExhaustiveReportC(Structure):
+    _fields_ = [("lo", c_float), ("hi", c_float), ("samples", c_uint64),
+                ("max_rel_err", c_double), ("mean_rel_err", c_double),
+                ("argmax_input", c_float), ("monotonic_violations", c_uint64),
+                ("first_violation", c_float), ("non_positive", c_uint64),
+                ("first_non_positive", c_float)]
+
+
+class ContinuityReportC(Structure):
+    _fields_ = [("worst_jump", c_double), ("at", c_float)]
+
+
+class GridAxisC(Structure):
+    _fields_ = [("lo", c_double), ("hi", c_double), ("step", c_double)]
+
+
+class GridSpecC(Structure):
+    _fields_ = [("a0", GridAxisC), ("a1", GridAxisC), ("a2", GridAxisC)]
+
+
+class GridResultC(Structure):
+    _fields_ = [("best", QuadCoeffsC), ("best_max_rel_err", c_double), ("step_a0", c_double),
+                ("step_a1", c_double), ("step_a2", c_double), ("points_searched", c_uint64)]
+
+
+class BiasResultC(Structure):
+    _fields_ = [("beta", c_float), ("max_rel_err", c_double), ("near_reference_bias", c_int32)]
 
 
 _fp = POINTER(c_float)
@@ -101,6 +148,22 @@ SIGNATURES = {
                                        _P, _P, _P]),
 }
 
+# mirrors include/quake_b200_lab.h
+LAB_SIGNATURES = {
+    "qk_sweep_spec_defaults": (SweepSpecC, []),
+    "qk_grid_spec_defaults": (GridSpecC, []),
+    "qk_lab_coeffs": (c_int, [POINTER(ExpConfigC), POINTER(AffineCoeffsC), POINTER(ClampRangeC)]),
+    "qk_sweep_error": (c_int, [POINTER(ExpConfigC), POINTER(SweepSpecC), POINTER(ErrorReportC)]),
+    "qk_sweep_exhaustive": (c_int, [POINTER(ExpConfigC), c_float, c_float,
+                                    POINTER(ExhaustiveReportC)]),
+    "qk_continuity_probe": (c_int, [POINTER(ExpConfigC), c_int32, c_int32,
+                                    POINTER(ContinuityReportC)]),
+    "qk_quad_max_rel_err": (c_int, [c_double, c_double, c_double, c_uint64, POINTER(c_double)]),
+    "qk_grid_search_quad": (c_int, [POINTER(GridSpecC), POINTER(GridResultC)]),
+    "qk_bias_reoptimize": (c_int, [POINTER(ExpConfigC), c_double, c_double,
+                                   POINTER(BiasResultC)]),
+}
+
 
 class QuakeLibraryMissing(ImportError):
     pass
@@ -118,7 +181,7 @@ def lib() -> ctypes.CDLL:
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                 "g.build()'` (or `make -C paper_2412_00408_b200/csrc`). There is no CPU fallback.")
         L = ctypes.CDLL(LIB_PATH)
-        for name, (res, args) in SIGNATURES.items():
+        for name, (res, args) in {**SIGNATURES, **LAB_SIGNATURES}.items():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -575,6 +575,10 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
 
 }  // namespace
 
+namespace qk {
+qk_status set_error(qk_status s, const std::string& msg) { return fail(s, msg); }
+}  // namespace qk
+
 // ===========================================================================
 extern "C" {
 

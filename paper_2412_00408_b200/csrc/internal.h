@@ -6,6 +6,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
+
+#include "quake_b200.h"
 
 namespace qk {
 
@@ -103,6 +106,9 @@ QK_SOFTMAX_LAUNCHER(quake2g)
 QK_SOFTMAX_LAUNCHER(quake_unfused)
 QK_SOFTMAX_LAUNCHER(quake2_unfused)
 #undef QK_SOFTMAX_LAUNCHER
+// Record `msg` as this thread's qk_last_error() and return `s` (host_api.cpp).
+qk_status set_error(qk_status s, const std::string& msg);
+
 int pipe_resident_probe(int variant, int cluster, int threads, size_t smem);
 
 cudaError_t launch_softmax(SmKernel k, const SmPlan& plan, const float* in, float* out,
