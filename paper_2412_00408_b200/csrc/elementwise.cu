@@ -164,6 +164,7 @@ template <EwOp OP, bool X86, int U>
 __global__ void __launch_bounds__(kThreads) ew_vec_kernel(const float* __restrict__ in,
                                                           float* __restrict__ out, size_t n,
                                                           size_t head, EwParams p) {
+  pdl_entry();
   const size_t n4 = (n - head) >> 2;
   const float4* __restrict__ in4 = reinterpret_cast<const float4*>(in + head);
   float4* __restrict__ out4 = reinterpret_cast<float4*>(out + head);
@@ -203,6 +204,7 @@ template <EwOp OP, bool X86, int U>
 __global__ void __launch_bounds__(kThreads) ew_scalar_kernel(const float* __restrict__ in,
                                                              float* __restrict__ out, size_t n,
                                                              EwParams p) {
+  pdl_entry();
   constexpr size_t kTile = static_cast<size_t>(kThreads) * U;
   for (size_t base = static_cast<size_t>(blockIdx.x) * kTile; base < n;
        base += static_cast<size_t>(gridDim.x) * kTile) {
@@ -236,17 +238,16 @@ cudaError_t launch_op(const float* in, float* out, size_t n, const EwParams& p, 
     size_t blocks = (n4 + static_cast<size_t>(kThreads) * U - 1) / (static_cast<size_t>(kThreads) * U);
     if (blocks > kMaxGrid) blocks = kMaxGrid;
     if (blocks == 0) blocks = 1;
-    ew_vec_kernel<OP, X86, U><<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(in, out, n, h,
-                                                                                      p);
+    return launch_ex(ew_vec_kernel<OP, X86, U>, dim3(static_cast<unsigned>(blocks)), dim3(kThreads),
+                     0, stream, 0, in, out, n, h, p);
   } else {
     constexpr int U = 8;
     size_t blocks = (n + static_cast<size_t>(kThreads) * U - 1) / (static_cast<size_t>(kThreads) * U);
     if (blocks > kMaxGrid) blocks = kMaxGrid;
     if (blocks == 0) blocks = 1;
-    ew_scalar_kernel<OP, X86, U><<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(in, out,
-                                                                                         n, p);
+    return launch_ex(ew_scalar_kernel<OP, X86, U>, dim3(static_cast<unsigned>(blocks)),
+                     dim3(kThreads), 0, stream, 0, in, out, n, p);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace

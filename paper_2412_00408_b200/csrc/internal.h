@@ -6,7 +6,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "quake_b200.h"
 
@@ -106,6 +108,43 @@ QK_SOFTMAX_LAUNCHER(quake2g)
 QK_SOFTMAX_LAUNCHER(quake_unfused)
 QK_SOFTMAX_LAUNCHER(quake2_unfused)
 #undef QK_SOFTMAX_LAUNCHER
+// Launch with programmatic stream serialization (PDL) unless QK_PDL=0, and
+// optionally as clusters of `cluster` CTAs (x). The kernels call pdl_entry().
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("QK_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t stream, unsigned cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  unsigned na = 0;
+  if (cluster > 0) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Record `msg` as this thread's qk_last_error() and return `s` (host_api.cpp).
 qk_status set_error(qk_status s, const std::string& msg);
 
