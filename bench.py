@@ -273,7 +273,7 @@ def main():
 
     peak, peak_kind = hbm_peak()
     achieved = BYTES_PER_ELEM * n_local / (kern_ms * 1e-3) / 1e9
-    plan = qk.softmax_plan(w.cols, True)
+    plan = qk.softmax_plan(w.cols, True, qk.KernelChoice.Quake2)
     kernel_name = {0: "softmax_warp_vec", 1: "softmax_warp_scalar", 2: "softmax_smem",
                    3: "softmax_global3", 4: "softmax_pipe (TMA pipeline, cluster)",
                    5: "softmax_pipe_la (lookahead TMA pipeline, cluster)"}[plan["variant"]]
@@ -301,8 +301,10 @@ def main():
     traffic = _load_traffic(w.name)
     if traffic:
         # DRAM bytes read + written per launch, from the committed ncu capture
-        line["roofline"]["traffic"] = traffic["bytes_per_launch"]
-        line["roofline"]["traffic_source"] = traffic["source"]
+        # (full matrix on one GPU; a rank's launch covers n_local / w.n of it)
+        line["roofline"]["traffic"] = traffic["bytes_per_launch"] * n_local / w.n
+        line["roofline"]["traffic_source"] = traffic["source"] + (
+            "" if world == 1 else f", scaled to this rank's {my_rows} rows")
     if rank == 0 and world == 1 and not args.no_extras:
         line["per_config"] = per_config(qk, L, _lib, peak)
         try:

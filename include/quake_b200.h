@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define QK_ABI_VERSION 1
+#define QK_ABI_VERSION 2
 
 typedef struct CUstream_st* qk_stream; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -144,7 +144,10 @@ int qk_quad_is_continuity_default(const qk_quad_coeffs* a);
 qk_gelu_constants qk_gelu_constants_defaults(void);
 int32_t qk_resolve_centering_bias(qk_kernel k, int32_t requested);
 const char* qk_kernel_name(qk_kernel k);
-qk_status qk_softmax_plan(size_t cols, int32_t aligned16, qk_softmax_plan_info* out);
+/* Launch geometry (and hence summation order) of softmax rows of `cols`
+ * columns for `kernel` on the current device. */
+qk_status qk_softmax_plan(size_t cols, int32_t aligned16, qk_kernel kernel,
+                          qk_softmax_plan_info* out);
 
 /* ---- 2. host-span operators (drop-ins for the std::span overloads) ---- */
 /* kernels.hpp:163-164 / kernels.cpp:95-107 quake_buffer */

@@ -12,7 +12,7 @@ from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int, c_in
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "libquake_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # qk_status
 QK_OK = 0
@@ -126,7 +126,7 @@ SIGNATURES = {
     "qk_gelu_constants_defaults": (GeluConstantsC, []),
     "qk_resolve_centering_bias": (c_int32, [c_int, c_int32]),
     "qk_kernel_name": (c_char_p, [c_int]),
-    "qk_softmax_plan": (c_int, [c_size_t, c_int32, POINTER(SoftmaxPlanC)]),
+    "qk_softmax_plan": (c_int, [c_size_t, c_int32, c_int, POINTER(SoftmaxPlanC)]),
     "qk_quake_buffer": (c_int, [_P, c_size_t, _P, c_size_t, POINTER(AffineCoeffsC),
                                 POINTER(ClampRangeC)]),
     "qk_quake2_buffer": (c_int, [_P, c_size_t, _P, c_size_t, POINTER(AffineCoeffsC),

@@ -104,9 +104,30 @@ __device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p) {
   if constexpr (X86 || !(OP == EwOp::kQuake || OP == EwOp::kQuake2 ||
                          OP == EwOp::kQuake2General || OP == EwOp::kLogisticQuake ||
                          OP == EwOp::kLogisticQuake2 || OP == EwOp::kGeluQuake ||
-                         OP == EwOp::kGeluQuake2)) {
+                         OP == EwOp::kGeluQuake2 || OP == EwOp::kGeluQuakeUnfused ||
+                         OP == EwOp::kGeluQuake2Unfused)) {
     a = apply<OP, X86>(a, p);
     b = apply<OP, X86>(b, p);
+  } else if constexpr (OP == EwOp::kGeluQuakeUnfused || OP == EwOp::kGeluQuake2Unfused) {
+    // w = (fs*x) * (ik + x*x): x*x feeds an add (scalar add), fs*x and the
+    // outer product feed no add, so all three products can be paired
+    float s0, s1, f0, f1;
+    unpack2(mul2_rn(pack2(a, b), pack2(a, b)), s0, s1);
+    unpack2(mul2_rn(pack2(p.k1, p.k1), pack2(a, b)), f0, f1);
+    float w0, w1;
+    unpack2(mul2_rn(pack2(f0, f1), pack2(__fadd_rn(p.k0, s0), __fadd_rn(p.k0, s1))), w0, w1);
+    w0 = saturate_fast(w0, p.lo, p.hi);
+    w1 = saturate_fast(w1, p.lo, p.hi);
+    float e0, e1;
+    if constexpr (OP == EwOp::kGeluQuakeUnfused) {
+      quake_body2(w0, w1, p.c0, p.c1, e0, e1);
+    } else {
+      quake2_body2<false>(w0, w1, p.c0, p.c1, 0.f, 0.f, 0.f, e0, e1);
+    }
+    const float y0 = __fdiv_rn(a, __fadd_rn(1.0f, e0));
+    const float y1 = __fdiv_rn(b, __fadd_rn(1.0f, e1));
+    a = y0 != y0 ? x86_quiet(a) : y0;
+    b = y1 != y1 ? x86_quiet(b) : y1;
   } else if constexpr (OP == EwOp::kGeluQuake || OP == EwOp::kGeluQuake2) {
     // u = x * (x*x + 1/kappa): the first product is added (scalar add), the
     // second feeds the clamp, so both products can be paired

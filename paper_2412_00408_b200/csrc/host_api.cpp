@@ -517,7 +517,8 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
     qk_status ss = ensure_workspace(st, nrows * cols);
     const float* dsrc_all = in_dev ? m + rb * cols : st.d_in;
     float* ddst_all = out_dev ? out + rb * cols : st.d_out;
-    const qk::SmPlan plan = qk::plan_softmax(cols, aligned16(dsrc_all) && aligned16(ddst_all), dev);
+    const qk::SmPlan plan =
+        qk::plan_softmax(cols, aligned16(dsrc_all) && aligned16(ddst_all), dev, sk);
     if (ss == QK_OK && cudaMemsetAsync(st.d_flags, 0, sizeof(uint32_t), st.streams[0]) != cudaSuccess) {
       ss = fail(QK_ERR_CUDA, "cudaMemset(flags)");
     }
@@ -685,9 +686,14 @@ const char* qk_kernel_name(qk_kernel k) {
   }
   return "unknown";
 }
-qk_status qk_softmax_plan(size_t cols, int32_t aligned, qk_softmax_plan_info* out) {
+qk_status qk_softmax_plan(size_t cols, int32_t aligned, qk_kernel kernel,
+                          qk_softmax_plan_info* out) {
   if (!out) return fail(QK_ERR_BAD_ARGUMENT, "softmax_plan: null pointer");
-  const qk::SmPlan p = qk::plan_softmax(cols, aligned != 0, current_device());
+  qk::SmKernel sk;
+  qk::SmParams sp;
+  qk_softmax_params prm{1.0f, -1, {1.0f / 3.0f, 0.0f, 2.0f / 3.0f}};
+  if (qk_status s = resolve_sm(&prm, kernel, &sk, &sp)) return s;
+  const qk::SmPlan p = qk::plan_softmax(cols, aligned != 0, current_device(), sk);
   out->variant = static_cast<int32_t>(p.variant);
   out->width = p.width;
   out->lanes = p.lanes;
@@ -769,8 +775,37 @@ qk_status qk_softmax_row(const float* v, size_t n, const qk_softmax_params* prm,
 }
 
 // ---- device operators ----
+// The library links cudart statically, so its current device is not the
+// caller's runtime's (e.g. torch's): launch on the device that owns the
+// stream (the legacy stream: the device holding the data), restoring the
+// previous device afterwards.
+class LaunchDevice {
+ public:
+  LaunchDevice(qk_stream stream, const void* data) {
+    cudaGetDevice(&prev_);
+    int dev = prev_;
+    if (stream != nullptr) {
+      if (cudaStreamGetDevice(reinterpret_cast<cudaStream_t>(stream), &dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = prev_;
+      }
+    } else if (!device_pointer(data, &dev)) {
+      dev = prev_;
+    }
+    if (dev != prev_ && cudaSetDevice(dev) == cudaSuccess) switched_ = true;
+  }
+  ~LaunchDevice() {
+    if (switched_) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = 0;
+  bool switched_ = false;
+};
+
 static qk_status launch_ew_device(const EwSpec& spec, const float* xs, float* out, size_t n,
                                   qk_stream stream) {
+  LaunchDevice on(stream, xs);
   const cudaError_t e = qk::launch_elementwise(spec.op, xs, out, n, spec.p,
                                                sm_count_of(current_device()),
                                                reinterpret_cast<cudaStream_t>(stream));
@@ -832,8 +867,9 @@ qk_status qk_softmax_rows_device(const float* matrix, size_t n, size_t cols,
   s = resolve_sm(prm, k, &sk, &sp);
   if (s != QK_OK) return s;
   const size_t rows = n / cols;
+  LaunchDevice on(stream, matrix);
   const qk::SmPlan plan =
-      qk::plan_softmax(cols, aligned16(matrix) && aligned16(out), current_device());
+      qk::plan_softmax(cols, aligned16(matrix) && aligned16(out), current_device(), sk);
   const cudaError_t e = qk::launch_softmax(sk, plan, matrix, out, rows, cols, sp, d_flags,
                                            reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? QK_OK : cuda_fail(e, "softmax kernel launch");

@@ -91,7 +91,8 @@ struct SmParams {
   int unfused;      // 1: kQuakeUnfused / kQuake2Unfused
 };
 
-SmPlan plan_softmax(size_t cols, bool aligned16, int device);
+// The plan depends on the kernel kind's arithmetic weight (see softmax.cu).
+SmPlan plan_softmax(size_t cols, bool aligned16, int device, SmKernel kind);
 
 // Launch softmax over `rows` rows of `cols` columns. `flags` (device, may be
 // null) receives bit 0 when a non-finite input was seen.

@@ -193,10 +193,13 @@ def clamp_for(c: AffineCoeffs) -> ClampRange:
     return ClampRange(F32(r.lo), F32(r.hi))
 
 
-def softmax_plan(cols: int, aligned16: bool = True) -> dict:
-    """Launch geometry the library picks for rows of `cols` columns."""
+def softmax_plan(cols: int, aligned16: bool = True,
+                 kernel: "KernelChoice" = None) -> dict:
+    """Launch geometry the library picks for rows of `cols` columns and the
+    given kernel choice (default Quake2); it fixes the summation order."""
     p = SoftmaxPlanC()
-    _check(_lib.lib().qk_softmax_plan(cols, int(aligned16), ctypes.byref(p)))
+    k = KernelChoice.Quake2 if kernel is None else kernel
+    _check(_lib.lib().qk_softmax_plan(cols, int(aligned16), int(k), ctypes.byref(p)))
     return {k: getattr(p, k) for k, _ in SoftmaxPlanC._fields_}
 
 

@@ -22,7 +22,8 @@ def time_plan(w, x, y, env, iters=10):
     L = _lib.lib()
     prm = qk.SoftmaxParams(temperature=w.temperature)._c()
     s = torch.cuda.current_stream().cuda_stream
-    fn = lambda: L.qk_softmax_rows_device(x.data_ptr(), w.n, w.cols, ctypes.byref(prm), 2,
+    kern = int(os.environ.get("SWEEP_KERNEL", "2"))
+    fn = lambda: L.qk_softmax_rows_device(x.data_ptr(), w.n, w.cols, ctypes.byref(prm), kern,
                                           y.data_ptr(), None, s)
     for _ in range(3):
         assert fn() == 0, _lib.last_error()
@@ -34,7 +35,7 @@ def time_plan(w, x, y, env, iters=10):
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / iters
-    return ms, qk.softmax_plan(w.cols)
+    return ms, qk.softmax_plan(w.cols, True, qk.KernelChoice(kern))
 
 
 def main():

@@ -152,7 +152,17 @@ def test_softmax_plan_geometry():
         # every thread owns KC-1 unconditional chunks, the last predicated
         assert p["threads"] % 32 == 0 and p["threads"] <= 512
         assert p["threads"] * (p["vpt"] - 1) <= q <= p["threads"] * p["vpt"]
-        assert p["stages"] >= 2 and p["smem"] <= 224 * 1024
+        assert p["stages"] >= 2 and p["smem"] <= 227 * 1024
+    # the plan follows the kernel's weight: at one CTA per row the light kinds
+    # take the fewest, fullest warps, the heavier ones the most warps
+    K = qk.KernelChoice
+    light = qk.softmax_plan(16384, True, K.Quake)
+    heavy = qk.softmax_plan(16384, True, K.Quake2)
+    assert (light["cluster"], light["threads"], light["vpt"]) == (1, 256, 16)
+    assert (heavy["cluster"], heavy["threads"], heavy["vpt"]) == (1, 512, 8)
+    assert qk.softmax_plan(16384, True, K.FastExp)["threads"] == 256
+    assert qk.softmax_plan(16384, True, K.Quake2Unfused)["threads"] == 512
+    assert qk.softmax_plan(16384, True, K.QuakeUnfused)["threads"] == 256
     for cols in (1025, 600000):
         p = qk.softmax_plan(cols)
         if p["variant"] == 2:

@@ -24,7 +24,7 @@ def test_unfused_softmax_bitexact(cols, kern):
     x = rng.uniform(-8, 8, rows * cols).astype(np.float32)  # bench.cpp:48-60 range
     x[: cols // 2] *= 20  # one row reaching the lower clamp of t*(x - m)
     xd = torch.from_numpy(x).cuda()
-    plan = qk.softmax_plan(cols, True)
+    plan = qk.softmax_plan(cols, True, K(kern))
     for t in (0.125, 0.7, 1.0, 4.0):
         y = qk.softmax_rows(xd, cols, qk.SoftmaxParams(temperature=t), K(kern)).cpu().numpy()
         assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern), f"{cols} {kern} {t}")
@@ -83,9 +83,10 @@ def test_fusion_ablation_softmax_and_validation():
                          temperature=0.7)
     r = ab.fusion_ablation(cfg)
     x = ab.fill_inputs(cfg).cpu().numpy()
-    plan = qk.softmax_plan(4096, True)
-    want = _rel(R.softmax_rows_ordered(x, 4096, plan, 0.7, QUAKE2),
-                R.softmax_rows_ordered(x, 4096, plan, 0.7, QUAKE2_UNFUSED))
+    fused_plan = qk.softmax_plan(4096, True, K.Quake2)
+    unfused_plan = qk.softmax_plan(4096, True, K.Quake2Unfused)
+    want = _rel(R.softmax_rows_ordered(x, 4096, fused_plan, 0.7, QUAKE2),
+                R.softmax_rows_ordered(x, 4096, unfused_plan, 0.7, QUAKE2_UNFUSED))
     assert r.max_rel_divergence == want
     assert 0 < r.max_rel_divergence < 1e-4
     with pytest.raises(ValueError, match="two warm-up"):

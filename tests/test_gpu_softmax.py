@@ -44,7 +44,7 @@ def test_shapes_bitexact_vs_ordered_restatement(cols, kernel):
     x = (np.random.default_rng(cols).standard_normal(rows * cols) * 3).astype(np.float32)
     for t in (0.125, 1.0):
         y = _gpu_softmax(x, cols, t, kernel)
-        plan = qk.softmax_plan(cols, True)
+        plan = qk.softmax_plan(cols, True, K(kernel))
         assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kernel),
                         f"cols={cols} k={kernel} t={t} plan={plan}")
         ref = R.softmax_rows(x, cols, t, kernel, sum_mode=1)  # fp64 row sum
@@ -56,9 +56,9 @@ def test_cfg4_full_size():
     R = restatement()
     xd = CFG4.device()
     x = xd.cpu().numpy()
-    plan = qk.softmax_plan(512, True)
     ref_lib = reference()
     for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(512, True, K(kern))
         p = qk.SoftmaxParams(temperature=CFG4.temperature)
         y = qk.softmax_rows(xd, 512, p, K(kern)).cpu().numpy()
         assert_bitexact(y, R.softmax_rows_ordered(x, 512, plan, CFG4.temperature, kern), "cfg4")
@@ -77,7 +77,7 @@ def test_cfg5_rows_and_full_properties():
     p = qk.SoftmaxParams(temperature=1.0)
     y = qk.softmax_rows(xd, cols, p, K.Quake2)
     torch.cuda.synchronize()
-    plan = qk.softmax_plan(cols, True)
+    plan = qk.softmax_plan(cols, True, K.Quake2)
     sub = slice(0, 64 * cols)
     xs = xd[sub].cpu().numpy()
     ys = y[sub].cpu().numpy()
@@ -101,11 +101,12 @@ def test_general_quad_and_bias_overrides():
     R = restatement()
     cols = 700
     x = (np.random.default_rng(5).standard_normal(40 * cols) * 2).astype(np.float32)
-    plan = qk.softmax_plan(cols, True)
+    plan = qk.softmax_plan(cols, True, K.Quake2)
     y = _gpu_softmax(x, cols, 0.5, QUAKE2, quad=MINIMAX)
     assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 0.5, QUAKE2, quad=MINIMAX), "minimax")
     for bias in (True, False):
         for kern in (QUAKE, QUAKE2):
+            plan = qk.softmax_plan(cols, True, K(kern))
             y = _gpu_softmax(x, cols, 2.0, kern, bias=bias)
             assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 2.0, kern, bias=int(bias)),
                             f"bias={bias} k={kern}")
@@ -119,7 +120,7 @@ def test_misaligned_rows_use_scalar_variants():
         xd = torch.from_numpy(base).cuda()[1:]  # 4-byte offset: not 16-byte aligned
         out = torch.empty(rows * cols + 1, device="cuda")[1:]
         qk.softmax_rows(xd, cols, qk.SoftmaxParams(), K.Quake2, out=out)
-        plan = qk.softmax_plan(cols, False)
+        plan = qk.softmax_plan(cols, False, K.Quake2)
         assert plan["width"] == 1
         assert_bitexact(out.cpu().numpy(), R.softmax_rows_ordered(base[1:], cols, plan, 1.0,
                                                                   QUAKE2), f"cols={cols}")
@@ -132,8 +133,8 @@ def test_extreme_rows_match_reference_conversion():
     x = np.concatenate([np.random.default_rng(1).uniform(-1e30, 1e30, cols),
                         np.random.default_rng(2).uniform(1e9, 2e9, cols),
                         np.random.default_rng(3).uniform(-5, 5, cols)]).astype(np.float32)
-    plan = qk.softmax_plan(cols, True)
     for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, True, K(kern))
         y = _gpu_softmax(x, cols, 1.0, kern)
         assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, kern), "extreme rows")
 
@@ -189,8 +190,8 @@ def test_interleaved_shapes_keep_launching():
         rows = 2 if cols > 100000 else 8
         x = (np.random.default_rng(cols).standard_normal(rows * cols) * 4).astype(np.float32)
         y = _gpu_softmax(x, cols, 1.0, QUAKE2)
-        assert_bitexact(y, R.softmax_rows_ordered(x, cols, qk.softmax_plan(cols, True), 1.0,
-                                                  QUAKE2), f"cols={cols}")
+        assert_bitexact(y, R.softmax_rows_ordered(x, cols, qk.softmax_plan(cols, True, K.Quake2),
+                                                  1.0, QUAKE2), f"cols={cols}")
 
 
 def test_large_host_path_validates_every_row_before_writeback():
