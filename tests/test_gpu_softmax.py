@@ -212,3 +212,17 @@ def test_large_host_path_validates_every_row_before_writeback():
         with pytest.raises(ValueError, match="softmax: non-finite input"):
             qk.softmax_rows(xb, cols, qk.SoftmaxParams(), K.Quake2, out=out)
         assert np.all(out == 123.0)
+
+
+@pytest.mark.parametrize("cols", [16384, 128256])
+def test_lookahead_variant_keeps_the_order(cols, monkeypatch):
+    """The experimental two-row-lookahead schedule (kPipeLA, QK_SM_LA=1) sums in the
+    same declared order: bit-exact against the ordered restatement of its plan."""
+    monkeypatch.setenv("QK_SM_LA", "1")
+    R = restatement()
+    plan = qk.softmax_plan(cols, True, K.Quake2)
+    assert plan["variant"] == 5
+    rows = 40
+    x = (np.random.default_rng(cols + 7).standard_normal(rows * cols) * 4).astype(np.float32)
+    y = _gpu_softmax(x, cols, 1.0, QUAKE2)
+    assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"LA cols={cols}")
