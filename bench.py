@@ -199,6 +199,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = _lib.lib()
+    # host-span calls (e2e) shard over the library's device list: this rank's GPU only
+    qk.set_devices([local])
     w = CONFIGS[args.workload]
     r0, r1 = row_shard(w.rows, rank, world)
     my_rows = r1 - r0
