@@ -41,6 +41,7 @@ import numpy as np  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 BYTES_PER_ELEM = 8         # 4 B read + 4 B write, every op
+SPEC_HBM_GBS = 8000.0      # B200 HBM3e spec (north star); reported beside the measured peak
 
 
 def hbm_peak():
@@ -142,6 +143,47 @@ def cpu_reference_rate(workload, rows_per_call: int, min_seconds: float, max_cal
                       f"(QuAKE2 softmax_rows), {len(times)} calls"}
 
 
+def cpu_single_thread(workload_name: str):
+    """The same CPU baseline with QUAKE_THREADS=1 (the reference caches its thread
+    count at first use, parallel.cpp:23-36, hence a child process)."""
+    env = dict(os.environ, QUAKE_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload",
+                              workload_name, "--cpu-rate-rows", "16"], env=env,
+                             capture_output=True, text=True, timeout=120)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
+
+
+def accuracy_report(qk, w, x, y):
+    """The approximation's error against true exp / true softmax (north star).
+    exp: every binary32 input of the kernel's clamp range, on the GPU lab
+    (include/quake_b200_lab.h). softmax: 8 rows of this workload's GPU output
+    against a binary64 softmax of the same inputs (numpy)."""
+    from paper_2412_00408_b200 import lab
+    out = {}
+    for name, kind, bias in (("quake", qk.KernelChoice.Quake, True),
+                             ("quake2", qk.KernelChoice.Quake2, False)):
+        cfg = lab.ExpConfig(kind, True, bias)
+        _, r = cfg.coeffs_and_clamp()
+        ex = lab.sweep_exhaustive(cfg, r.lo, r.hi)
+        out[f"{name}_exp_vs_exp"] = {"max_rel_err": ex.max_rel_err, "mean_rel_err": ex.mean_rel_err,
+                                     "inputs": ex.samples, "range": [r.lo, r.hi],
+                                     "monotonic_violations": ex.monotonic_violations}
+    rows = 8
+    xs = x[: rows * w.cols].view(rows, w.cols).double().cpu().numpy()
+    ys = y[: rows * w.cols].view(rows, w.cols).double().cpu().numpy()
+    z = xs * w.temperature
+    e = np.exp(z - z.max(axis=1, keepdims=True))
+    truth = e / e.sum(axis=1, keepdims=True)
+    rel = np.abs(ys - truth) / truth
+    out["softmax_vs_fp64_softmax"] = {"max_rel_err": float(rel.max()),
+                                      "mean_rel_err": float(rel.mean()),
+                                      "sample": f"{rows} rows of {w.name}"}
+    return out
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -182,7 +224,14 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--no-extras", action="store_true", help="skip per_config and cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-rate-rows", type=int, default=0,
+                    help=argparse.SUPPRESS)  # internal: print the CPU baseline rate and exit
     args = ap.parse_args()
+    if args.cpu_rate_rows:
+        from paper_2412_00408_b200.workloads import CONFIGS
+        r = cpu_reference_rate(CONFIGS[args.workload], args.cpu_rate_rows, 3.0, 40)
+        print(json.dumps({k: r[k] for k in ("kind", "cores", "value", "sample")}))
+        return 0
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -245,6 +294,9 @@ def main():
     assert int(flags.item()) == 0, "non-finite flag raised on finite input"
     region_ms = region0.elapsed_time(region1)
     launch_ms = [a.elapsed_time(b) for a, b in ev]
+    launch_min_ms = min(launch_ms)
+    # input fingerprint: sum of the fp32 bit patterns as int64 (stated algorithm)
+    fingerprint = int(x.view(torch.int32).sum(dtype=torch.int64).item())
     t = torch.tensor([region_ms, float(np.mean(launch_ms))], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -288,12 +340,16 @@ def main():
                    "temperature": w.temperature, "rows_per_gpu": my_rows,
                    "distribution": "N(0,4) seed 5 (torch CUDA Philox)",
                    "l2": "inputs (2.1 GB) larger than L2 (126 MB); no flush needed",
+                   "input_fingerprint": {"value": fingerprint,
+                                         "algorithm": "sum of this rank's fp32 bit patterns "
+                                                      "as int32, accumulated in int64"},
                    "plan": plan},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
                      "peak_kind": peak_kind, "kernel": kernel_name,
                      "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n_local,
-                     "avg_launch_us": kern_ms * 1e3},
+                     "avg_launch_us": kern_ms * 1e3, "min_launch_us": launch_min_ms * 1e3,
+                     "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS},
         "e2e": {"value": e2e_value, "unit": "elements/s",
                 "h2d_bytes_per_step": 4 * total_elems, "d2h_bytes_per_step": 4 * total_elems,
                 "path": "qk_softmax_rows (host-span C-ABI), pinned host buffers"},
@@ -316,6 +372,8 @@ def main():
                                     "sample": cb["sample"]}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(e)}
+        line["cpu_baseline"]["single_thread"] = cpu_single_thread(w.name)
+        line["accuracy"] = accuracy_report(qk, w, x, y)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
