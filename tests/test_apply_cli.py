@@ -135,3 +135,69 @@ def test_apply_softmax_rows_and_errors(tmp_path):
             "--output", str(tmp_path / "o2.raw"))
     assert r.returncode == 2 and "non-finite" in r.stderr
     assert not (tmp_path / "o2.raw").exists()
+
+
+# ---- the reference's CLI cases (tests/test_cli.cpp:73-229) on quake_apply ----
+
+@pytest.mark.gpu
+def test_reference_cli_cases(tmp_path):
+    inp, out = tmp_path / "in.csv", tmp_path / "out.csv"
+    # apply softmax to a uniform row (test_cli.cpp:73-83)
+    inp.write_text("0\n0\n0\n0\n")
+    assert run("apply", "--op", "softmax", "--input", str(inp), "--output", str(out)).returncode == 0
+    assert list(read_csv(out)) == [0.25] * 4
+    # apply gelu maps zero to zero (:85-94)
+    inp.write_text("0\n")
+    assert run("apply", "--op", "gelu", "--input", str(inp), "--output", str(out)).returncode == 0
+    assert list(read_csv(out)) == [0.0]
+    # apply exp with the biased first-order kernel (:96-107)
+    inp.write_text("1.0\n")
+    assert run("apply", "--op", "exp", "--kernel", "quake", "--bias", "on", "--input", str(inp),
+               "--output", str(out)).returncode == 0
+    y = read_csv(out)
+    assert y.size == 1 and abs(y[0] - np.e) / np.e <= 0.043
+    # csv reader accepts commas and newlines (test_io.cpp:77-86)
+    inp.write_text("1.5, 2.5\n3.5,\n4.5\n")
+    assert run("apply", "--op", "exp", "--kernel", "exact", "--input", str(inp),
+               "--output", str(out)).returncode == 0
+    assert read_csv(out).size == 4
+    # exact softmax through apply is stable under reapplication (:211-229)
+    inp.write_text("0.25\n0.25\n0.25\n0.25\n")
+    once, twice = tmp_path / "once.csv", tmp_path / "twice.csv"
+    assert run("apply", "--op", "softmax", "--kernel", "exact", "--input", str(inp),
+               "--output", str(once)).returncode == 0
+    assert run("apply", "--op", "softmax", "--kernel", "exact", "--input", str(once),
+               "--output", str(twice)).returncode == 0
+    a, b = read_csv(once), read_csv(twice)
+    assert np.all(np.abs(a - b) <= 2 * np.spacing(a))
+
+
+def test_reference_cli_validation(tmp_path):
+    """test_cli.cpp:109-123: shape, missing file, junk token, unknown op."""
+    inp = tmp_path / "in.csv"
+    inp.write_text("1\n2\n3\n")
+    assert run("apply", "--op", "softmax", "--cols", "2", "--input", str(inp), "--output",
+               str(tmp_path / "o.csv")).returncode == 2
+    assert run("apply", "--op", "exp", "--input", str(tmp_path / "missing.csv"), "--output",
+               str(tmp_path / "o.csv")).returncode == 3
+    inp.write_text("1, banana\n")
+    assert run("apply", "--op", "exp", "--input", str(inp), "--output",
+               str(tmp_path / "o.csv")).returncode == 2
+    assert run("apply", "--op", "transmogrify", "--input", str(inp), "--output", "x").returncode == 2
+
+
+@pytest.mark.gpu
+def test_raw_round_trip_is_deterministic(tmp_path):
+    """test_cli.cpp:175-209: two runs (and a different device list) give identical bytes."""
+    x = np.random.default_rng(97).uniform(-5, 5, 257).astype(np.float32)
+    inp = tmp_path / "in.qak"
+    write_raw(inp, x)
+    outs = []
+    for i, extra in enumerate(([], [], ["--devices", "0"])):
+        o = tmp_path / f"o{i}.qak"
+        r = run("apply", "--op", "logistic", "--kernel", "quake2", "--format", "raw",
+                "--input", str(inp), "--output", str(o), *extra)
+        assert r.returncode == 0, r.stderr
+        outs.append(o.read_bytes())
+    assert outs[0] == outs[1] == outs[2]
+    assert_bitexact(read_raw(tmp_path / "o0.qak"), restatement().logistic_buffer(x, QUAKE2))
