@@ -28,7 +28,6 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
-import math
 from dataclasses import asdict, dataclass, field
 from typing import Callable, List, Optional
 
@@ -91,6 +90,18 @@ class AblationReport:
     fusion_speedup: float
     max_rel_divergence: float
     divergence_note: str = field(default="max |a-b|/max(|a|,|b|) over elements, fp64")
+
+
+def workload_name(w: str) -> str:
+    """bench.cpp:385-397 (workloads are their names here)."""
+    if w not in WORKLOADS:
+        return "unknown"
+    return w
+
+
+def workload_from_name(name: str) -> Optional[str]:
+    """bench.cpp:399-405."""
+    return name if name in WORKLOADS else None
 
 
 def element_count(cfg: BenchConfig) -> int:
@@ -202,14 +213,14 @@ def fusion_ablation(cfg: BenchConfig) -> AblationReport:
     """bench.cpp:425-513 fusion_ablation."""
     if cfg.workload not in ("softmax_matrix", "gelu_vector"):
         raise ValueError("fusion_ablation: workload must be softmax_matrix or gelu_vector")
-    if cfg.kernel not in UNFUSED:
-        raise ValueError("fusion_ablation: kernel must be quake or quake2")
     validate(cfg)
     x = fill_inputs(cfg)
     y_f = torch.empty_like(x)
     y_u = torch.empty_like(x)
     fused = make_pass(cfg, cfg.kernel, x, y_f)
-    unfused = make_pass(cfg, UNFUSED[cfg.kernel], x, y_u)
+    # kernels without an affine fold (Exact, expf, __expf) run the same pass twice
+    # (bench.cpp:95-100: "the exact path ignores fusion")
+    unfused = make_pass(cfg, UNFUSED.get(cfg.kernel, cfg.kernel), x, y_u)
     for _ in range(cfg.warmup_iters):
         fused()
         unfused()

@@ -95,6 +95,8 @@ def test_fusion_ablation_softmax_and_validation():
         ab.run_bench(ab.BenchConfig(measured_iters=9))
     with pytest.raises(ValueError, match="softmax_matrix or gelu_vector"):
         ab.fusion_ablation(ab.BenchConfig(workload="exp_vector"))
+    with pytest.raises(ValueError, match="empty workload"):
+        ab.run_bench(ab.BenchConfig(n=0))
 
 
 def test_run_bench_and_kernel_matrix():
@@ -107,3 +109,38 @@ def test_run_bench_and_kernel_matrix():
     # Exact against itself through the same scaffolding: ~1 (bench.hpp:67-72)
     ex = [r for r in reps if r.kernel == "exact"]
     assert all(0.5 < r.speedup_vs_exact < 2.0 for r in ex)
+
+
+# ---- the reference's bench cases (tests/test_bench.cpp), GPU-adapted bounds ----
+
+def test_reference_bench_cases():
+    # run_bench produces a coherent report (test_bench.cpp:25-42); on a bandwidth-bound
+    # chip QuAKE does not beat exp by > 1x, so only positivity of the ratio is required
+    r = ab.run_bench(ab.BenchConfig(workload="exp_vector", n=1 << 18, kernel=K.Quake))
+    assert (r.workload, r.kernel, r.elements) == ("exp_vector", "quake", 1 << 18)
+    assert 0 < r.min_seconds <= r.mean_seconds and r.throughput_eps > 0
+    assert np.isfinite(r.checksum) and r.speedup_vs_exact > 0
+    # self-comparison lands near unity (:44-55)
+    r = ab.run_bench(ab.BenchConfig(workload="exp_vector", n=1 << 24, kernel=K.Exact,
+                                    measured_iters=12))
+    assert 0.85 < r.speedup_vs_exact < 1.18
+    # identical fused and unfused kernels time the same (:94-105)
+    a = ab.fusion_ablation(ab.BenchConfig(workload="softmax_matrix", rows=8192, cols=1024,
+                                          kernel=K.Exact, measured_iters=12))
+    assert 0.85 < a.fusion_speedup < 1.18 and a.max_rel_divergence == 0.0
+    # fusion keeps values put (:75-92): within 2e-5
+    a = ab.fusion_ablation(ab.BenchConfig(workload="softmax_matrix", rows=256, cols=512,
+                                          kernel=K.Quake))
+    assert a.fused.fused and not a.unfused.fused and a.max_rel_divergence <= 2e-5
+    a = ab.fusion_ablation(ab.BenchConfig(workload="gelu_vector", n=100_000, kernel=K.Quake2))
+    assert a.max_rel_divergence <= 2e-5
+    # mean time scales with the workload (:107-120), at bandwidth-bound sizes
+    small = ab.run_bench(ab.BenchConfig(workload="exp_vector", n=1 << 25, kernel=K.Quake2,
+                                        measured_iters=12))
+    big = ab.run_bench(ab.BenchConfig(workload="exp_vector", n=1 << 26, kernel=K.Quake2,
+                                      measured_iters=12))
+    assert 1.6 <= big.mean_seconds / small.mean_seconds <= 2.6
+    # workload names round-trip (:122-129)
+    for w in ab.WORKLOADS:
+        assert ab.workload_from_name(ab.workload_name(w)) == w
+    assert ab.workload_from_name("matmul") is None
