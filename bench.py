@@ -11,14 +11,16 @@ across the N GPUs of the job (strong scaling; no data-path collective). A
            (qk_softmax_rows) from pinned host memory: H2D + kernel + D2H
            inside the timed region;
   roofline — algorithmic bytes (8 B/element: one read, one write) per launch
-           over the average launch duration (CUDA events), against the
-           measured HBM copy peak in MEASURED_PEAKS.json;
+           over the average launch duration (timed region / K, CUDA events
+           on the launch stream), against the measured HBM copy peak in
+           MEASURED_PEAKS.json; isolated per-launch event timings beside it;
   cpu_baseline — the reference's own softmax_rows (oracle/_ref, compiled in
            place from the reference sources) on a bounded row sample, all
            host threads, rank 0 at N=1 only.
   per_config — rank 0 at N=1: every BASELINE config and kernel choice
-           (QuAKE, QuAKE2, expf, __expf) timed the same way, L2 flushed
-           between launches.
+           (QuAKE, QuAKE2, expf, __expf) and a same-size copy, rotating
+           through input/output pairs >= 4x L2 so no launch reads cached
+           input; back-to-back and isolated launch times.
 
 `--impl reference` times the reference's CPU implementation instead (rank 0
 only; other ranks exit 0).
@@ -278,21 +280,29 @@ def main():
         for _ in range(args.warmup):
             launch()
     barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     region0, region1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        # the timed region holds exactly K back-to-back launches of the kernel
+        # (no events between them, so each launch's start overlaps the previous
+        # drain under PDL): region / K is the kernel's average launch duration
         with torch.cuda.stream(stream):
             region0.record(stream)
             for i in range(args.steps):
-                ev[i][0].record(stream)
                 launch()
-                ev[i][1].record(stream)
             region1.record(stream)
         barrier()
     assert int(flags.item()) == 0, "non-finite flag raised on finite input"
     region_ms = region0.elapsed_time(region1)
+    # untimed afterwards: the same launches each bracketed by an event pair
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            launch()
+            ev[i][1].record(stream)
+    barrier()
     launch_ms = [a.elapsed_time(b) for a, b in ev]
     launch_min_ms = min(launch_ms)
     # input fingerprint: sum of the fp32 bit patterns as int64 (stated algorithm)
@@ -300,7 +310,8 @@ def main():
     t = torch.tensor([region_ms, float(np.mean(launch_ms))], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    region_ms, kern_ms = t.tolist()
+    region_ms, iso_ms = t.tolist()
+    kern_ms = region_ms / args.steps
     total_elems = w.n if world > 1 else n_local
     value = total_elems * args.steps / (region_ms * 1e-3)
 
@@ -348,7 +359,10 @@ def main():
                      "frac": achieved / peak, "traffic": None,
                      "peak_kind": peak_kind, "kernel": kernel_name,
                      "algorithmic_bytes_per_launch": BYTES_PER_ELEM * n_local,
-                     "avg_launch_us": kern_ms * 1e3, "min_launch_us": launch_min_ms * 1e3,
+                     "avg_launch_us": kern_ms * 1e3,
+                     "avg_launch_source": "timed region / steps (K back-to-back launches, "
+                                          "CUDA events on the launch stream)",
+                     "isolated_launch_us": {"mean": iso_ms * 1e3, "min": launch_min_ms * 1e3},
                      "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS},
         "e2e": {"value": e2e_value, "unit": "elements/s",
                 "h2d_bytes_per_step": 4 * total_elems, "d2h_bytes_per_step": 4 * total_elems,
@@ -399,6 +413,8 @@ def per_config(qk, L, _lib, peak, iters=12):
     (evicted) and pays for writing back the previous launches' dirty output,
     as a kernel inside a real pipeline would. (A flush-then-launch timing
     would let a 64 MB output finish in L2 and flatter the small configs.)
+    `us`/`frac` are the back-to-back (pipelined) launch time; `*_isolated`
+    bracket every launch with its own event pair.
     """
     import torch
     from paper_2412_00408_b200.workloads import CFG1, CFG2, CFG3, CFG4
@@ -408,20 +424,41 @@ def per_config(qk, L, _lib, peak, iters=12):
     K = qk.KernelChoice
     l2 = 126 << 20
 
-    def timeit(fns):
-        evs = []
+    def timeit(fns, reps=4):
+        """(back-to-back, isolated) mean seconds per launch.
+
+        back-to-back: one event pair around reps*len(fns) queued launches, so
+        each launch's start-up overlaps the previous one's drain (PDL) as in a
+        pipeline of operators; isolated: an event pair around every launch,
+        which serialises launch latency, ramp and drain into each interval.
+        """
         with torch.cuda.stream(stream):
-            for i in range(iters + len(fns)):
+            for f in fns:  # warm
+                if f() != 0:
+                    raise RuntimeError(_lib.last_error())
+            a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                for f in fns:
+                    f()
+            b0.record(stream)
+            evs = []
+            for i in range(iters):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                st = fns[i % len(fns)]()
+                fns[i % len(fns)]()
                 b.record(stream)
-                if st != 0:
-                    raise RuntimeError(_lib.last_error())
-                if i >= len(fns):
-                    evs.append((a, b))
+                evs.append((a, b))
         stream.synchronize()
-        return float(np.mean([a.elapsed_time(b) for a, b in evs])) * 1e-3
+        b2b = a0.elapsed_time(b0) * 1e-3 / (reps * len(fns))
+        return b2b, float(np.mean([a.elapsed_time(b) for a, b in evs])) * 1e-3
+
+    def entry(s, n):
+        b2b, iso = s
+        g, gi = BYTES_PER_ELEM * n / b2b / 1e9, BYTES_PER_ELEM * n / iso / 1e9
+        return {"us": b2b * 1e6, "elements_per_s": n / b2b, "gbps": g, "frac": g / peak,
+                "us_isolated": iso * 1e6, "gbps_isolated": gi, "frac_isolated": gi / peak,
+                "rotation_buffers": pairs}
 
     for w in (CFG1, CFG2, CFG3, CFG4):
         n = w.n
@@ -436,9 +473,8 @@ def per_config(qk, L, _lib, peak, iters=12):
                 return 0
             return f
         sc = timeit([copy_fn(x, y) for x, y in zip(xs, ys)])
-        res[f"{w.name}:copy_reference"] = {"us": sc * 1e6, "gbps": BYTES_PER_ELEM * n / sc / 1e9,
-                                           "frac": BYTES_PER_ELEM * n / sc / 1e9 / peak,
-                                           "rotation_buffers": pairs}
+        res[f"{w.name}:copy_reference"] = {k: v for k, v in entry(sc, n).items()
+                                           if k != "elements_per_s"}
         for kn in ("quake", "quake2", "expf", "fast_expf"):
             k = int({"quake": K.Quake, "quake2": K.Quake2, "expf": K.Expf,
                      "fast_expf": K.FastExp}[kn])
@@ -457,10 +493,7 @@ def per_config(qk, L, _lib, peak, iters=12):
                                                         ctypes.byref(prm), k, y.data_ptr(),
                                                         None, sh)
 
-            s = timeit([make(x, y) for x, y in zip(xs, ys)])
-            gbs = BYTES_PER_ELEM * n / s / 1e9
-            res[f"{w.name}:{kn}"] = {"us": s * 1e6, "elements_per_s": n / s, "gbps": gbs,
-                                     "frac": gbs / peak, "rotation_buffers": pairs}
+            res[f"{w.name}:{kn}"] = entry(timeit([make(x, y) for x, y in zip(xs, ys)]), n)
         del xs, ys
         torch.cuda.empty_cache()
     return res

@@ -89,6 +89,7 @@ struct SmParams {
   int general_quad; // 1: y_m may leave [1, 2]; rows use SSE-exact semantics
   float nat_c0, nat_c1, nat_lo, nat_hi;  // unfused kinds: natural-exp coefficients / clamp
   int unfused;      // 1: kQuakeUnfused / kQuake2Unfused
+  int pdl_late;     // persistent kernels: trigger the dependent launch after the last row
 };
 
 // The plan depends on the kernel kind's arithmetic weight (see softmax.cu).
@@ -115,6 +116,17 @@ inline bool pdl_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("QK_PDL");
     return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// Persistent (one-wave) kernels: trigger the dependent launch after the last
+// row instead of at entry, so the next grid's CTAs do not take the slots of
+// this grid's early finishers (QK_PDL_LATE=0 restores the entry trigger).
+inline int pdl_late_enabled() {
+  static const int on = [] {
+    const char* v = std::getenv("QK_PDL_LATE");
+    return (v && v[0] == '0') ? 0 : 1;
   }();
   return on;
 }
