@@ -3,6 +3,10 @@
 For each row length, times (back to back, ~4.2 GB moved per launch) the
 planner's default plan and the single-stage schedule (QK_SM_STAGES=1) at each
 feasible cluster size, and checks every row sums to 1 within 1e-4.
+
+The single-stage schedule was measured with this script, rejected
+(profiles/r01_single_stage_long_rows.jsonl) and removed from
+the kernel; QK_SM_STAGES=1 now leaves only the default rows.
 """
 import ctypes
 import json
