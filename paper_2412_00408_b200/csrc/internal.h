@@ -64,6 +64,7 @@ enum class SmVariant : int {
   kGlobal3 = 3,     // CTA per row, three sweeps over global memory (huge rows)
   kPipe = 4,        // persistent cluster per row group, multi-stage TMA pipeline
   kPipeLA = 5,      // kPipe with the cluster exchange awaited one row late
+  kPipeL2 = 6,      // long rows: one smem stage, next rows prefetched into L2
 };
 
 struct SmPlan {

@@ -10,8 +10,11 @@ cudaError_t launch_softmax_quake2(const SmPlan& plan, const float* in, float* ou
 }
 
 // Clusters of the persistent pipelines resident at once for one launch shape
-// (the planner's occupancy probe; variant 4 = kPipe, 5 = kPipeLA).
+// (the planner's occupancy probe; variant 4 = kPipe, 5 = kPipeLA, 6 = kPipeL2).
 int pipe_resident_probe(int variant, int cluster, int threads, size_t smem) {
+  if (variant == 6) {
+    return resident_clusters(softmax_pipe_l2<SmKernel::kQuake2, 16>, cluster, threads, smem);
+  }
   return variant == 5 ? resident_clusters(softmax_pipe_la<SmKernel::kQuake2, 8>, cluster, threads, smem)
                       : resident_clusters(softmax_pipe<SmKernel::kQuake2, true, 16>, cluster, threads,
                                           smem);
