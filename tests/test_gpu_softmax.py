@@ -226,3 +226,59 @@ def test_lookahead_variant_keeps_the_order(cols, monkeypatch):
     x = (np.random.default_rng(cols + 7).standard_normal(rows * cols) * 4).astype(np.float32)
     y = _gpu_softmax(x, cols, 1.0, QUAKE2)
     assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"LA cols={cols}")
+
+
+@pytest.mark.parametrize("cols", [202048, 262144, 300000])
+def test_long_row_pipeline_is_default_and_bitexact(cols):
+    """Long vocab rows take the one-stage long-row pipeline (kPipeL2) and keep the
+    declared order: bit-exact against the ordered restatement of its plan, with
+    more rows than resident clusters so every cluster runs several rows (stage
+    refills, both exchange parities)."""
+    R = restatement()
+    plan = qk.softmax_plan(cols, True, K.Quake2)
+    assert plan["variant"] == 6 and plan["stages"] == 1, plan
+    rows = 2 * plan["resident"] + 3
+    x = (np.random.default_rng(cols + 11).standard_normal(rows * cols) * 4).astype(np.float32)
+    y = _gpu_softmax(x, cols, 1.0, QUAKE2)
+    assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"L2 cols={cols}")
+    assert max_rel(y, R.softmax_rows(x, cols, 1.0, QUAKE2, sum_mode=1)) <= TOL
+
+
+@pytest.mark.parametrize("cols,pf", [(16384, "0"), (128256, "0"), (128256, "2"), (50000, "1")])
+def test_long_row_pipeline_forced_keeps_the_order(cols, pf, monkeypatch):
+    """kPipeL2 forced (QK_SM_L2=1) on shorter rows, with and without L2 bulk
+    prefetch: both kernel kinds, both temperatures, bit-exact."""
+    monkeypatch.setenv("QK_SM_L2", "1")
+    monkeypatch.setenv("QK_SM_PF", pf)
+    R = restatement()
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, True, K(kern))
+        assert plan["variant"] == 6, plan
+        rows = min(3 * plan["resident"] + 1, (1 << 24) // cols)
+        x = (np.random.default_rng(cols + 3).standard_normal(rows * cols) * 3).astype(np.float32)
+        for t in (0.125, 1.0):
+            y = _gpu_softmax(x, cols, t, kern)
+            assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
+                            f"forced L2 cols={cols} k={kern} t={t} pf={pf}")
+
+
+def test_long_row_pipeline_extreme_and_non_finite_rows(monkeypatch):
+    """kPipeL2 rows on the x86-emulation path (huge magnitudes) and the clamp path
+    stay bit-exact; a non-finite value in any row raises the flag."""
+    R = restatement()
+    cols = 262144
+    rng = np.random.default_rng(4)
+    rows = [rng.uniform(-1e30, 1e30, cols), rng.uniform(1e9, 2e9, cols),
+            rng.standard_normal(cols) * 40, rng.standard_normal(cols)]
+    x = np.concatenate(rows).astype(np.float32)
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, True, K(kern))
+        assert plan["variant"] == 6
+        y = _gpu_softmax(x, cols, 1.0, kern)
+        assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, kern), f"extreme L2 k={kern}")
+    for bad in (np.nan, np.inf):
+        xb = x.copy()
+        xb[3 * cols + 77] = bad
+        xd = torch.from_numpy(xb).cuda()
+        with pytest.raises(ValueError, match="non-finite"):
+            qk.softmax_rows(xd, cols, qk.SoftmaxParams(), K.Quake2)
