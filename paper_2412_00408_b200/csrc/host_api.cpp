@@ -785,7 +785,13 @@ class LaunchDevice {
     cudaGetDevice(&prev_);
     int dev = prev_;
     if (stream != nullptr) {
-      if (cudaStreamGetDevice(reinterpret_cast<cudaStream_t>(stream), &dev) != cudaSuccess) {
+      const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        // cudaStreamGetDevice invalidates a stream capture (CUDA graphs):
+        // while capturing, take the device that holds the data
+        if (!device_pointer(data, &dev)) dev = prev_;
+      } else if (cudaStreamGetDevice(s, &dev) != cudaSuccess) {
         cudaGetLastError();
         dev = prev_;
       }
