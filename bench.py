@@ -63,54 +63,94 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled during the timed region.
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML (nvidia-ml-py) is polled every ~2 ms from a thread, so even a 13 ms
+    timed region gets several samples; the caller marks the region with
+    begin()/end() and only samples taken inside it are summarised. Falls back
+    to polling nvidia-smi when NVML is unavailable.
+    """
 
-    def __init__(self, gpu_index: int):
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active")
+
+    def __init__(self, gpu_index: int, uuid: str | None = None):
         self.gpu = gpu_index
-        self.samples = []
+        self.samples = []  # (t, sm_mhz, max_mhz, reasons_mask)
+        self.window = [None, None]
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            if uuid:
+                try:
+                    h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+                except Exception:
+                    h = None
+            self._h = h if h is not None else pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+        self.source = "nvml" if self._nvml else "nvidia-smi"
+
+    def _sample(self):
+        if self._nvml:
+            nv = self._nvml
+            sm = float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            mask = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            return sm, self._max, mask
+        out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        f = [v.strip() for v in out.split(",")]
+        return float(f[1]), float(f[2]), int(f[4], 16)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
+                sm, mx, mask = self._sample()
+                self.samples.append((time.perf_counter(), sm, mx, mask))
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._ready.set()
+            self._stop.wait(0.002 if self._nvml else 0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(10)  # sampling is live before the timed region starts
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
 
+    def begin(self):
+        self.window[0] = time.perf_counter()
+
+    def end(self):
+        self.window[1] = time.perf_counter()
+
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
-                    "samples": 0}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for i, nm in enumerate(names):
-                if len(s) > 5 + i and s[5 + i].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+        t0, t1 = self.window
+        inside = [s for s in self.samples
+                  if (t0 is None or s[0] >= t0) and (t1 is None or s[0] <= t1)]
+        used = inside or self.samples[-1:]
+        if not used:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"],
+                    "samples": 0, "source": self.source}
+        reasons = sorted({nm for _, _, _, m in used for nm, bit in self.REASONS if m & bit})
+        return {"sm_mhz": float(np.median([s[1] for s in used])),
+                "sm_max_mhz": max(s[2] for s in used), "reasons": reasons,
+                "samples": len(inside), "source": self.source,
+                "window_ms": None if t0 is None or t1 is None else (t1 - t0) * 1e3}
 
 
 # ---------------------------------------------------------------------------
@@ -281,8 +321,13 @@ def main():
             launch()
     barrier()
     region0, region1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    except Exception:
+        uuid = None
+    with ClockSampler(local, uuid) as clk:
         barrier()
+        clk.begin()
         # the timed region holds exactly K back-to-back launches of the kernel
         # (no events between them, so each launch's start overlaps the previous
         # drain under PDL): region / K is the kernel's average launch duration
@@ -292,6 +337,7 @@ def main():
                 launch()
             region1.record(stream)
         barrier()
+        clk.end()
     assert int(flags.item()) == 0, "non-finite flag raised on finite input"
     region_ms = region0.elapsed_time(region1)
     # untimed afterwards: the same launches each bracketed by an event pair
