@@ -172,10 +172,12 @@ def test_non_finite_rejected_and_out_untouched():
         qk.softmax_rows(xd, 512, qk.SoftmaxParams(), K.Quake2)
 
 
-def test_exact_kernel_close_to_reference():
+@pytest.mark.parametrize("cols", [512, 128256, 262144])
+def test_exact_kernel_close_to_reference(cols):
+    """Exact (expf) softmax through every pipeline (warp, two-stage, long-row)."""
     R = restatement()
-    cols = 512
-    x = (np.random.default_rng(9).standard_normal(64 * cols) * 2).astype(np.float32)
+    rows = max(4, min(64, (1 << 21) // cols))
+    x = (np.random.default_rng(9).standard_normal(rows * cols) * 2).astype(np.float32)
     from oracle.oracle import EXACT
     y = _gpu_softmax(x, cols, 0.125, EXACT)
     assert max_rel(y, R.softmax_rows(x, cols, 0.125, EXACT, sum_mode=1)) <= 1e-5
