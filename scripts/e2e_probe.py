@@ -1,0 +1,26 @@
+"""Probe (not product): timeline of one host-span cfg5 softmax call (QK_HOST_SCAN_DEBUG=1
+prints when the host scan and the device checks decided), next to the raw PCIe rates."""
+import ctypes
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2412_00408_b200 as qk  # noqa: E402
+from paper_2412_00408_b200 import _lib  # noqa: E402
+from paper_2412_00408_b200.workloads import CFG5  # noqa: E402
+
+L = _lib.lib()
+x = CFG5.device()
+hx = x.cpu().pin_memory()
+hy = torch.empty_like(hx).pin_memory()
+prm = qk.SoftmaxParams()._c()
+for i in range(4):
+    t0 = time.perf_counter()
+    st = L.qk_softmax_rows(hx.data_ptr(), hx.numel(), CFG5.cols, ctypes.byref(prm), 2,
+                           hy.data_ptr(), hy.numel())
+    dt = time.perf_counter() - t0
+    print(f"call {i}: status {st} {dt * 1e3:.1f} ms -> {hx.numel() / dt / 1e9:.2f} Gelem/s",
+          file=sys.stderr, flush=True)

@@ -197,23 +197,27 @@ def test_interleaved_shapes_keep_launching():
 
 
 def test_large_host_path_validates_every_row_before_writeback():
-    """Host span > one pipeline chunk: rows are validated on the host while the
-    upload runs and results stream back overlapped (host_api.cpp) — a bad value in
-    the last chunk must still leave `out` untouched, and clean results equal the
-    device path bit for bit (nonlin.cpp:176-180)."""
+    """Host span > one pipeline chunk: every chunk is validated by the device max
+    pass before any result is copied back (host_api.cpp). A bad value anywhere —
+    first, middle or last chunk — must leave `out` untouched, and clean results
+    equal the device path bit for bit (nonlin.cpp:176-180)."""
     cols = 65536
-    rows = 300  # 19.7M elements > the 16M-element chunk
+    rows = 600  # 39.3M elements: three 16M-element chunks
     x = (np.random.default_rng(17).standard_normal(rows * cols) * 4).astype(np.float32)
     y = qk.softmax_rows(x, cols, qk.SoftmaxParams(), K.Quake2)
     yd = qk.softmax_rows(torch.from_numpy(x).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
     assert_bitexact(y, yd.cpu().numpy(), "host overlap path vs device path")
-    for bad in (np.nan, np.inf):
-        xb = x.copy()
-        xb[-3] = bad
-        out = np.full_like(xb, 123.0)
-        with pytest.raises(ValueError, match="softmax: non-finite input"):
-            qk.softmax_rows(xb, cols, qk.SoftmaxParams(), K.Quake2, out=out)
-        assert np.all(out == 123.0)
+    for pos in (5, rows * cols // 2 + 1, rows * cols - 3):
+        for bad in (np.nan, np.inf, -np.inf):
+            xb = x.copy()
+            xb[pos] = bad
+            out = np.full_like(xb, 123.0)
+            with pytest.raises(ValueError, match="softmax: non-finite input"):
+                qk.softmax_rows(xb, cols, qk.SoftmaxParams(), K.Quake2, out=out)
+            assert np.all(out == 123.0), (pos, bad)
+    # the library stays usable after a rejected call
+    y2 = qk.softmax_rows(x, cols, qk.SoftmaxParams(), K.Quake2)
+    assert_bitexact(y2, y, "after a rejected call")
 
 
 @pytest.mark.parametrize("cols", [16384, 128256])
