@@ -1,5 +1,8 @@
-"""Probe (not product): timeline of one host-span cfg5 softmax call (QK_HOST_SCAN_DEBUG=1
-prints when the host scan and the device checks decided), next to the raw PCIe rates."""
+"""Probe (not product): wall time of host-span cfg5 softmax calls (pinned buffers).
+
+The log in profiles/r01_e2e_host_scan_probe.log was taken with a since-removed
+host-scan variant whose QK_HOST_SCAN_DEBUG=1 output shows when the scan and
+the device check decided."""
 import ctypes
 import os
 import sys
