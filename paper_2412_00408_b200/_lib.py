@@ -11,7 +11,8 @@ from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int, c_in
                     c_size_t, c_uint32, c_uint64, c_void_p)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libquake_b200.so")
+# QK_LIB_PATH: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("QK_LIB_PATH") or os.path.join(PKG_DIR, "libquake_b200.so")
 ABI_VERSION = 2
 
 # qk_status
