@@ -64,7 +64,8 @@ enum class SmVariant : int {
   kGlobal3 = 3,     // CTA per row, three sweeps over global memory (huge rows)
   kPipe = 4,        // persistent cluster per row group, multi-stage TMA pipeline
   kPipeLA = 5,      // kPipe with the cluster exchange awaited one row late
-  kPipeL2 = 6,      // long rows: one smem stage, next rows prefetched into L2
+  kPipeL2 = 6,      // long rows: one smem stage, prefix refilled under the exps
+  kPipeS = 7,       // kPipe with one-float chunks: rows of cols % 4 != 0 (unaligned)
 };
 
 struct SmPlan {

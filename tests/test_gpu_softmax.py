@@ -126,10 +126,11 @@ def test_misaligned_rows_use_scalar_variants():
                                                                   QUAKE2), f"cols={cols}")
 
 
-def test_extreme_rows_match_reference_conversion():
-    """Huge-magnitude rows: the reference's cvttss2si out-of-range behaviour is emulated."""
+@pytest.mark.parametrize("cols", [64, 63, 1001, 50257])
+def test_extreme_rows_match_reference_conversion(cols):
+    """Huge-magnitude rows: the reference's cvttss2si out-of-range behaviour is emulated
+    (float4 and scalar-lane kernels: cols % 4 != 0 rows are not 16-byte aligned)."""
     R = restatement()
-    cols = 64
     x = np.concatenate([np.random.default_rng(1).uniform(-1e30, 1e30, cols),
                         np.random.default_rng(2).uniform(1e9, 2e9, cols),
                         np.random.default_rng(3).uniform(-5, 5, cols)]).astype(np.float32)
@@ -137,6 +138,26 @@ def test_extreme_rows_match_reference_conversion():
         plan = qk.softmax_plan(cols, True, K(kern))
         y = _gpu_softmax(x, cols, 1.0, kern)
         assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, kern), "extreme rows")
+
+
+@pytest.mark.parametrize("cols", [7, 63, 257, 1001, 4097, 50257])
+def test_unaligned_rows_clamp_and_division_paths(cols):
+    """Rows of cols % 4 != 0 (scalar lanes): narrow rows (no element reaches v_min:
+    clamp-free exps, proven fast division), wide rows (clamped tails, quotients near
+    the subnormal range: checked division), both kinds and temperatures."""
+    R = restatement()
+    rng = np.random.default_rng(cols)
+    rows = max(4, min(48, (1 << 21) // cols))
+    narrow = rng.standard_normal(rows * cols)
+    wide = rng.uniform(-300, 40, rows * cols)
+    for x in (narrow, wide):
+        x = x.astype(np.float32)
+        for kern in (QUAKE, QUAKE2):
+            plan = qk.softmax_plan(cols, cols % 4 == 0, K(kern))
+            for t in (0.125, 1.0):
+                y = _gpu_softmax(x, cols, t, kern)
+                assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
+                                f"cols={cols} k={kern} t={t}")
 
 
 def test_reference_properties():
