@@ -388,7 +388,8 @@ def main():
     kernel_name = {0: "softmax_warp_vec", 1: "softmax_warp_scalar", 2: "softmax_smem",
                    3: "softmax_global3", 4: "softmax_pipe (TMA pipeline, cluster)",
                    5: "softmax_pipe_la (lookahead TMA pipeline, cluster)",
-                   6: "softmax_pipe_l2 (long-row pipeline, cluster)"}[plan["variant"]]
+                   6: "softmax_pipe_l2 (long-row pipeline, cluster)",
+                   7: "softmax_pipe_s (scalar-lane pipeline, cluster)"}[plan["variant"]]
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,

@@ -106,7 +106,8 @@ typedef struct {
 typedef struct {
   int32_t variant; /* 0 warp/float4, 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep,
                       4 persistent TMA pipeline (+cluster), 5 its lookahead form,
-                      6 long-row pipeline (one stage, prefix refilled early) */
+                      6 long-row pipeline (one stage, prefix refilled early),
+                      7 scalar-lane pipeline (cols % 4 != 0) */
   int32_t width;   /* elements per chunk: 4 or 1 */
   int32_t lanes;   /* partial-sum lanes per CTA */
   int32_t cluster; /* CTAs per row */
@@ -114,10 +115,10 @@ typedef struct {
   int32_t threads; /* CTA size */
   int32_t vpt;     /* warp variants: chunks per lane */
   int64_t smem;    /* dynamic smem bytes per CTA */
-  int32_t stages;  /* variants 4-6: row slices staged per CTA */
+  int32_t stages;  /* variants 4-7: row slices staged per CTA */
   int32_t balanced;/* 1: CTA r's slice is q (+1 for r < nchunks % cluster) chunks;
                       0: `slice` chunks per CTA, the last one short */
-  int32_t resident;/* variants 4-6: clusters resident at once on this device (0 = unknown) */
+  int32_t resident;/* variants 4-7: clusters resident at once on this device (0 = unknown) */
 } qk_softmax_plan_info;
 
 /* ---- library ---- */
