@@ -389,7 +389,8 @@ def main():
                    3: "softmax_global3", 4: "softmax_pipe (TMA pipeline, cluster)",
                    5: "softmax_pipe_la (lookahead TMA pipeline, cluster)",
                    6: "softmax_pipe_l2 (long-row pipeline, cluster)",
-                   7: "softmax_pipe_s (scalar-lane pipeline, cluster)"}[plan["variant"]]
+                   7: "softmax_pipe_s (scalar-lane pipeline, cluster)",
+                   8: "softmax_warp_multi (short rows, several per warp)"}[plan["variant"]]
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,

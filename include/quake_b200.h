@@ -107,7 +107,8 @@ typedef struct {
   int32_t variant; /* 0 warp/float4, 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep,
                       4 persistent TMA pipeline (+cluster), 5 its lookahead form,
                       6 long-row pipeline (one stage, prefix refilled early),
-                      7 scalar-lane pipeline (cols % 4 != 0) */
+                      7 scalar-lane pipeline (cols % 4 != 0),
+                      8 several short rows per warp (lanes = lanes per row) */
   int32_t width;   /* elements per chunk: 4 or 1 */
   int32_t lanes;   /* partial-sum lanes per CTA */
   int32_t cluster; /* CTAs per row */

@@ -66,6 +66,7 @@ enum class SmVariant : int {
   kPipeLA = 5,      // kPipe with the cluster exchange awaited one row late
   kPipeL2 = 6,      // long rows: one smem stage, prefix refilled under the exps
   kPipeS = 7,       // kPipe with one-float chunks: rows of cols % 4 != 0 (unaligned)
+  kWarpMulti = 8,   // 32/G short rows per warp, G lanes each (order of kWarpVec/kWarpScalar)
 };
 
 struct SmPlan {

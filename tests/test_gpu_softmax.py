@@ -309,3 +309,34 @@ def test_long_row_pipeline_extreme_and_non_finite_rows(monkeypatch):
         xd = torch.from_numpy(xb).cuda()
         with pytest.raises(ValueError, match="non-finite"):
             qk.softmax_rows(xd, cols, qk.SoftmaxParams(), K.Quake2)
+
+
+@pytest.mark.parametrize("cols", [1, 2, 3, 4, 5, 7, 8, 12, 15, 16, 17, 24, 31, 32, 33, 48, 63, 64,
+                                  65])
+def test_short_rows_several_per_warp(cols):
+    """Rows of <= 16 chunks run 32/G rows per warp (kWarpMulti) with the warp-per-row
+    order: bit-exact against the ordered restatement, with a row count that leaves
+    dead lanes in the last warp, and x86-emulated (huge-magnitude), clamped and
+    ordinary rows interleaved so neighbouring rows in one warp take different paths."""
+    R = restatement()
+    rng = np.random.default_rng(cols + 100)
+    rows = 1003
+    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+    x[1::7] = rng.uniform(-1e30, 1e30, (len(x[1::7]), cols))  # x86 conversion rows
+    x[2::7] = rng.uniform(1e9, 2e9, (len(x[2::7]), cols))
+    x[3::7] = rng.uniform(-300, 40, (len(x[3::7]), cols))      # clamped tails
+    x = x.ravel()
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, cols % 4 == 0, K(kern))
+        for t in (0.125, 1.0):
+            y = _gpu_softmax(x, cols, t, kern)
+            assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
+                            f"cols={cols} k={kern} t={t} plan={plan}")
+    from oracle.oracle import EXACT
+    y = _gpu_softmax(x[: 40 * cols] / 1e20 if cols > 0 else x, cols, 1.0, EXACT)
+    assert np.all(np.isfinite(y))
+    # a non-finite value in one row of a packed warp raises the flag
+    xb = x.copy()
+    xb[5 * cols] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
