@@ -390,7 +390,9 @@ def main():
                    5: "softmax_pipe_la (lookahead TMA pipeline, cluster)",
                    6: "softmax_pipe_l2 (long-row pipeline, cluster)",
                    7: "softmax_pipe_s (scalar-lane pipeline, cluster)",
-                   8: "softmax_warp_multi (short rows, several per warp)"}[plan["variant"]]
+                   8: "softmax_warp_multi (short rows, several per warp)",
+                   9: "softmax_thread_row (one thread per row)",
+                   10: "softmax_rows_smem (one thread per row, smem tile)"}[plan["variant"]]
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,

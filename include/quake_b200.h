@@ -108,7 +108,9 @@ typedef struct {
                       4 persistent TMA pipeline (+cluster), 5 its lookahead form,
                       6 long-row pipeline (one stage, prefix refilled early),
                       7 scalar-lane pipeline (cols % 4 != 0),
-                      8 several short rows per warp (lanes = lanes per row) */
+                      8 several short rows per warp (lanes = lanes per row),
+                      9 one thread per row (<= 16 cols; lanes = 1: sequential sum),
+                      10 one thread per row through an smem tile (lanes = 1) */
   int32_t width;   /* elements per chunk: 4 or 1 */
   int32_t lanes;   /* partial-sum lanes per CTA */
   int32_t cluster; /* CTAs per row */

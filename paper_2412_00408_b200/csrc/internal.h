@@ -67,6 +67,8 @@ enum class SmVariant : int {
   kPipeL2 = 6,      // long rows: one smem stage, prefix refilled under the exps
   kPipeS = 7,       // kPipe with one-float chunks: rows of cols % 4 != 0 (unaligned)
   kWarpMulti = 8,   // 32/G short rows per warp, G lanes each (order of kWarpVec/kWarpScalar)
+  kThreadRow = 9,   // one thread per row (<= 16 cols): the reference's sequential order
+  kRowsSmem = 10,   // one thread per row, rows staged through smem (coalesced), <= 64 cols
 };
 
 struct SmPlan {

@@ -332,6 +332,10 @@ def test_short_rows_several_per_warp(cols):
             y = _gpu_softmax(x, cols, t, kern)
             assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
                             f"cols={cols} k={kern} t={t} plan={plan}")
+            if plan["variant"] == 9:  # one thread per row: the reference's own order
+                assert plan["lanes"] == 1
+                assert_bitexact(y, R.softmax_rows(x, cols, t, kern, sum_mode=0),
+                                f"thread-per-row vs the reference's sequential sum, cols={cols}")
     from oracle.oracle import EXACT
     y = _gpu_softmax(x[: 40 * cols] / 1e20 if cols > 0 else x, cols, 1.0, EXACT)
     assert np.all(np.isfinite(y))
@@ -340,3 +344,25 @@ def test_short_rows_several_per_warp(cols):
     xb[5 * cols] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
         qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
+
+
+@pytest.mark.parametrize("cols", [1, 3, 8, 17, 31, 32, 33, 48, 63, 64])
+def test_rows_staged_in_smem_sequential_order(cols, monkeypatch):
+    """kRowsSmem (one thread per row, rows staged through shared memory) keeps the
+    reference's sequential order: bit-exact against the reference-order restatement
+    for a row count that ends in a partial CTA, with x86 and clamped rows mixed in."""
+    monkeypatch.setenv("QK_SM_ROWSMEM", "1")
+    R = restatement()
+    rng = np.random.default_rng(cols + 7)
+    rows = 700
+    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
+    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
+    x = x.ravel()
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, cols % 4 == 0, K(kern))
+        assert plan["variant"] == 10 and plan["lanes"] == 1
+        for t in (0.125, 1.0):
+            y = _gpu_softmax(x, cols, t, kern)
+            assert_bitexact(y, R.softmax_rows(x, cols, t, kern, sum_mode=0),
+                            f"rows-smem vs the reference's sequential sum, cols={cols} t={t}")
