@@ -252,7 +252,10 @@ cudaError_t launch_op(const float* in, float* out, size_t n, const EwParams& p, 
   const uintptr_t ao = reinterpret_cast<uintptr_t>(out) & 15u;
   const bool vec = ai == ao && (ai & 3u) == 0;
   if (vec) {
-    constexpr int U = 4;
+#ifndef QK_EW_U
+#define QK_EW_U 4
+#endif
+    constexpr int U = QK_EW_U;
     const size_t head = ai == 0 ? 0 : (16u - ai) / 4u;
     const size_t h = head < n ? head : n;
     const size_t n4 = (n - h) / 4;
