@@ -134,7 +134,7 @@ std::vector<int> active_devices() {
 
 struct DeviceState {
   std::mutex mu;  // serialises host-span calls on this device
-  int sm_count = 0;
+  std::atomic<int> sm_count{0};  // read lock-free by concurrent launches
   float* d_in = nullptr;
   float* d_out = nullptr;
   size_t cap = 0;  // floats
@@ -144,19 +144,18 @@ struct DeviceState {
 
 constexpr int kMaxDevices = 64;
 DeviceState g_state[kMaxDevices];
-std::mutex g_sm_mu;
 
 int sm_count_of(int dev) {
   DeviceState& st = g_state[dev];
-  if (st.sm_count == 0) {
-    std::lock_guard<std::mutex> lk(g_sm_mu);
-    int v = 0;
+  int v = st.sm_count.load(std::memory_order_acquire);
+  if (v == 0) {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
       v = 148;
     }
-    st.sm_count = v;
+    st.sm_count.store(v, std::memory_order_release);
   }
-  return st.sm_count;
+  return v;
 }
 
 int current_device() {
