@@ -419,7 +419,8 @@ def main():
                    7: "softmax_pipe_s (scalar-lane pipeline, cluster)",
                    8: "softmax_warp_multi (short rows, several per warp)",
                    9: "softmax_thread_row (one thread per row)",
-                   10: "softmax_rows_smem (one thread per row, smem tile)"}[plan["variant"]]
+                   10: "softmax_rows_smem (one thread per row, smem tile)",
+                   11: "softmax_subwarp (G lanes per row)"}[plan["variant"]]
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,

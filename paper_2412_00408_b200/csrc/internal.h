@@ -69,6 +69,7 @@ enum class SmVariant : int {
   kWarpMulti = 8,   // 32/G short rows per warp, G lanes each (order of kWarpVec/kWarpScalar)
   kThreadRow = 9,   // one thread per row (<= 16 cols): the reference's sequential order
   kRowsSmem = 10,   // one thread per row, rows staged through smem (coalesced), <= 64 cols
+  kSubWarp = 11,    // G lanes per aligned row, up to 8 float4 chunks each (lanes = G)
 };
 
 struct SmPlan {

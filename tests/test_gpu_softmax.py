@@ -366,3 +366,25 @@ def test_rows_staged_in_smem_sequential_order(cols, monkeypatch):
             y = _gpu_softmax(x, cols, t, kern)
             assert_bitexact(y, R.softmax_rows(x, cols, t, kern, sum_mode=0),
                             f"rows-smem vs the reference's sequential sum, cols={cols} t={t}")
+
+
+@pytest.mark.parametrize("cols", [20, 32, 64, 100, 128, 256, 512, 1000, 1024])
+def test_subwarp_rows_keep_the_declared_order(cols, monkeypatch):
+    """kSubWarp (G lanes per aligned row, chunks l, l+G, ... per lane; QK_SM_SUBWARP=1):
+    bit-exact against the ordered restatement of its plan, x86 and clamped rows
+    interleaved, a partial last warp."""
+    monkeypatch.setenv("QK_SM_SUBWARP", "1")
+    R = restatement()
+    rng = np.random.default_rng(cols + 31)
+    rows = 509
+    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
+    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
+    x = x.ravel()
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, True, K(kern))
+        assert plan["variant"] == 11, plan
+        for t in (0.125, 1.0):
+            y = _gpu_softmax(x, cols, t, kern)
+            assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
+                            f"subwarp cols={cols} k={kern} t={t} plan={plan}")
