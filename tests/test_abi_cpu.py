@@ -137,8 +137,17 @@ def test_empty_inputs_are_noops():
 
 
 def test_softmax_plan_geometry():
-    p = qk.softmax_plan(512)
-    assert (p["variant"], p["width"], p["lanes"], p["vpt"]) == (0, 4, 32, 4)
+    p = qk.softmax_plan(512)  # cfg4: 16 lanes per row, 8 float4 chunks each
+    assert (p["variant"], p["width"], p["lanes"], p["vpt"]) == (11, 4, 16, 8)
+    for cols in (20, 32, 64, 128, 1000, 1024):  # sub-warp rows cover every chunk
+        p = qk.softmax_plan(cols)
+        assert p["variant"] == 11 and p["lanes"] * p["vpt"] * 4 >= cols, (cols, p)
+        assert p["lanes"] & (p["lanes"] - 1) == 0 and 2 <= p["lanes"] <= 32
+    for cols, aligned in ((4, True), (16, True), (7, False), (10, False)):
+        p = qk.softmax_plan(cols, aligned)  # one thread per row: the sequential order
+        assert (p["variant"], p["lanes"]) == (9, 1), (cols, p)
+    p = qk.softmax_plan(31, False)  # unaligned 11-48: one thread per row via smem
+    assert (p["variant"], p["lanes"], p["width"]) == (10, 1, 1)
     p = qk.softmax_plan(513, False)
     assert (p["variant"], p["width"]) == (1, 1)
     p = qk.softmax_plan(1 << 23)
