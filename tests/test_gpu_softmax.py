@@ -388,3 +388,25 @@ def test_subwarp_rows_keep_the_declared_order(cols, monkeypatch):
             y = _gpu_softmax(x, cols, t, kern)
             assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
                             f"subwarp cols={cols} k={kern} t={t} plan={plan}")
+
+
+@pytest.mark.parametrize("cols", [49, 77, 197, 257, 513, 577, 1001, 1023])
+def test_subwarp_scalar_rows_keep_the_declared_order(cols, monkeypatch):
+    """Scalar-lane sub-warp rows (G lanes per unaligned row; default for 49-96
+    columns, forced up to 1024 with QK_SM_SUBWARP_S=1):
+    bit-exact against the ordered restatement, x86 and clamped rows interleaved."""
+    monkeypatch.setenv("QK_SM_SUBWARP_S", "1")
+    R = restatement()
+    rng = np.random.default_rng(cols + 41)
+    rows = 389
+    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
+    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
+    x = x.ravel()
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, False, K(kern))
+        assert plan["variant"] == 11 and plan["width"] == 1, plan
+        for t in (0.125, 1.0):
+            y = _gpu_softmax(x, cols, t, kern)
+            assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
+                            f"subwarp-s cols={cols} k={kern} t={t} plan={plan}")
