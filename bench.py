@@ -420,7 +420,8 @@ def main():
                    8: "softmax_warp_multi (short rows, several per warp)",
                    9: "softmax_thread_row (one thread per row)",
                    10: "softmax_rows_smem (one thread per row, smem tile)",
-                   11: "softmax_subwarp (G lanes per row)"}[plan["variant"]]
+                   11: "softmax_subwarp (G lanes per row)",
+                   12: "softmax_tiles (TMA row tiles)"}[plan["variant"]]
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,

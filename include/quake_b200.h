@@ -111,7 +111,8 @@ typedef struct {
                       8 several short rows per warp (lanes = lanes per row),
                       9 one thread per row (<= 16 cols; lanes = 1: sequential sum),
                       10 one thread per row through an smem tile (lanes = 1),
-                      11 G lanes per aligned row (lanes = G, vpt = chunks per lane) */
+                      11 G lanes per row (lanes = G, vpt = chunks per lane),
+                      12 TMA row tiles, G lanes per row (unaligned 97-128 cols) */
   int32_t width;   /* elements per chunk: 4 or 1 */
   int32_t lanes;   /* partial-sum lanes per CTA */
   int32_t cluster; /* CTAs per row */

@@ -70,6 +70,7 @@ enum class SmVariant : int {
   kThreadRow = 9,   // one thread per row (<= 16 cols): the reference's sequential order
   kRowsSmem = 10,   // one thread per row, rows staged through smem (coalesced), <= 64 cols
   kSubWarp = 11,    // G lanes per aligned row, up to 8 float4 chunks each (lanes = G)
+  kTiles = 12,      // unaligned rows in TMA row tiles through smem, G lanes per row
 };
 
 struct SmPlan {

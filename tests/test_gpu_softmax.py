@@ -410,3 +410,28 @@ def test_subwarp_scalar_rows_keep_the_declared_order(cols, monkeypatch):
             y = _gpu_softmax(x, cols, t, kern)
             assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
                             f"subwarp-s cols={cols} k={kern} t={t} plan={plan}")
+
+
+@pytest.mark.parametrize("cols", [97, 127, 197, 257, 513, 577, 1001, 1023])
+@pytest.mark.parametrize("rows", [1, 37, 389])
+def test_row_tiles_keep_the_declared_order(cols, rows, monkeypatch):
+    """kTiles (TMA row tiles through smem for unaligned rows, G lanes per row;
+    default for 97-128 columns, forced up to 1024 with QK_SM_TILES=1): bit-exact against the ordered restatement with full tiles, a
+    partial last tile and a single row; x86 and clamped rows interleaved."""
+    monkeypatch.setenv("QK_SM_TILES", "1")
+    R = restatement()
+    rng = np.random.default_rng(cols * 7 + rows)
+    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
+    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
+    x = x.ravel()
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, False, K(kern))
+        assert plan["variant"] == 12 and plan["width"] == 1, plan
+        y = _gpu_softmax(x, cols, 1.0, kern)
+        assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, kern),
+                        f"tiles cols={cols} rows={rows} k={kern} plan={plan}")
+    xb = x.copy()
+    xb[-1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
