@@ -435,3 +435,19 @@ def test_row_tiles_keep_the_declared_order(cols, rows, monkeypatch):
     xb[-1] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
         qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
+
+
+@pytest.mark.parametrize("cols", [7, 16, 31, 77, 127, 128, 257, 512, 1001, 4097, 16384, 50257,
+                                  128256, 262144])
+def test_in_place_matches_out_of_place(cols):
+    """out aliasing the input (as the reference's span API permits): every kernel
+    family reads a row (or tile) completely before writing it, so in-place results
+    equal out-of-place ones bit for bit."""
+    rows = max(3, min(200, (1 << 22) // cols))
+    x = torch.randn(rows * cols, device="cuda", generator=torch.Generator("cuda").manual_seed(cols)) * 3
+    p = qk.SoftmaxParams(temperature=0.5)
+    y = qk.softmax_rows(x, cols, p, K.Quake2)
+    xi = x.clone()
+    qk.softmax_rows(xi, cols, p, K.Quake2, out=xi)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32), xi.view(torch.int32)), cols
