@@ -1,5 +1,5 @@
 """One launch each of the cfg2 logistic QuAKE2, cfg3 GELU QuAKE2 and cfg4
-softmax QuAKE2 kernels (device API), for ncu captures."""
+softmax QuAKE2 kernels (device API; cfg4 runs softmax_subwarp), for ncu captures."""
 import ctypes
 import os
 import sys
