@@ -16,7 +16,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:soft
 echo "ncu pipe exit $?" >> gpurun_out/ncu_full.log
 CMD2="python scripts/kernel_probe.py"
 timeout 300 $CMD2 > gpurun_out/kernel_probe.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none -k regex:"ew_vec_kernel|softmax_warp_vec|softmax_subwarp" -c 3 -o /tmp/prof_ew -f $CMD2 > gpurun_out/ncu_ew.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:"ew_vec_kernel|softmax_warp_vec|softmax_subwarp" -c 6 -o /tmp/prof_ew -f $CMD2 > gpurun_out/ncu_ew.log 2>&1
 echo "ncu ew exit $?" >> gpurun_out/ncu_ew.log
 # summaries only (the full reports would exceed gpurun's 64 MiB copy-back)
 python scripts/ncu_summary.py /tmp/prof_ew.ncu-rep gpurun_out/ncu_ew_summary "elementwise + warp softmax" > /dev/null 2>&1
