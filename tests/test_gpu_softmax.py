@@ -412,11 +412,11 @@ def test_subwarp_scalar_rows_keep_the_declared_order(cols, monkeypatch):
                             f"subwarp-s cols={cols} k={kern} t={t} plan={plan}")
 
 
-@pytest.mark.parametrize("cols", [97, 127, 197, 257, 513, 577, 1001, 1023])
+@pytest.mark.parametrize("cols", [97, 127, 129, 161, 197, 257, 513, 577, 1001, 1023])
 @pytest.mark.parametrize("rows", [1, 37, 389])
 def test_row_tiles_keep_the_declared_order(cols, rows, monkeypatch):
     """kTiles (TMA row tiles through smem for unaligned rows, G lanes per row;
-    default for 97-128 columns, forced up to 1024 with QK_SM_TILES=1): bit-exact against the ordered restatement with full tiles, a
+    default for 97-200 columns, forced up to 1024 with QK_SM_TILES=1): bit-exact against the ordered restatement with full tiles, a
     partial last tile and a single row; x86 and clamped rows interleaved."""
     monkeypatch.setenv("QK_SM_TILES", "1")
     R = restatement()
