@@ -15,15 +15,26 @@ across the N GPUs of the job (strong scaling; no data-path collective). A
            on the launch stream), against the measured HBM copy peak in
            MEASURED_PEAKS.json; isolated per-launch event timings beside it;
   cpu_baseline — the reference's own softmax_rows (oracle/_ref, compiled in
-           place from the reference sources) on a bounded row sample, all
-           host threads, rank 0 at N=1 only.
+           place from the reference sources) on the full cfg5 matrix (the
+           same bytes), all host threads, rank 0 at N=1 only; beside it the
+           same with QUAKE_THREADS=1 on a row sample.
   per_config — rank 0 at N=1: every BASELINE config and kernel choice
            (QuAKE, QuAKE2, expf, __expf) and a same-size copy, rotating
            through input/output pairs >= 4x L2 so no launch reads cached
-           input; back-to-back and isolated launch times.
+           input; back-to-back and isolated launch times; and the reference's
+           own CPU functions (quake_buffer / quake2_buffer / logistic_buffer /
+           gelu_buffer / softmax_rows) on the identical bytes, all threads and
+           QUAKE_THREADS=1.
+
+Inputs come from the counter-based generator in workloads.py: a rank's rows
+are the same bytes as that slice of the single-GPU draw, so per-rank input
+fingerprints add up to the N=1 fingerprint and so do the output ones (the
+results do not depend on the GPU count). Ranks share nothing on the data
+path; a gloo group carries only the barrier and the max-over-ranks timing.
 
 `--impl reference` times the reference's CPU implementation instead (rank 0
-only; other ranks exit 0).
+only; other ranks exit 0): exactly `--steps` calls of softmax_rows over the
+full cfg5 matrix after `--warmup` calls, all host threads.
 """
 from __future__ import annotations
 
@@ -156,45 +167,122 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # reference arm / CPU baseline
 
-def cpu_reference_rate(workload, rows_per_call: int, min_seconds: float, max_calls: int,
-                       warmup: int = 1):
-    """Time the reference's own softmax_rows (or the restatement if the reference
-    was not built) on `rows_per_call` rows of the workload; returns a dict."""
-    from oracle.oracle import QUAKE, QUAKE2, best_cpu_baseline
-    impl = best_cpu_baseline()
-    cols = workload.cols
-    x = workload.host(rows_per_call * cols).reshape(rows_per_call, cols)
+def host_info():
+    """Host the CPU baseline ran on (nproc, CPU model, arch)."""
+    import platform
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "arch": platform.machine()}
+
+
+def _fp(a) -> int:
+    """Fingerprint: the fp32 bit patterns read as int32, summed in int64."""
+    return int(np.asarray(a, dtype=np.float32).view(np.int32).astype(np.int64).sum())
+
+
+def cpu_op(impl, w, kern: str):
+    """(fn(x, out), label) calling the reference's own buffer API for workload w
+    (kernels.cpp:95-136, nonlin.cpp:162-330); exp as `quake apply --op exp`
+    (quake_cli.cpp:277-289: natural-exp coefficients, per-kernel bias)."""
+    from oracle.oracle import CONTINUITY, QUAKE, QUAKE2
+    k = QUAKE if kern == "quake" else QUAKE2
+    if w.op == "exp":
+        c0, c1 = impl.named_coeffs("natural", k == QUAKE)
+        lo, hi = impl.clamp_for(c0, c1)
+        if k == QUAKE:
+            return (lambda x, o: impl.quake_buffer(x, c0, c1, lo, hi, out=o)), "quake_buffer"
+        return (lambda x, o: impl.quake2_buffer(x, c0, c1, CONTINUITY, lo, hi, out=o)), \
+            "quake2_buffer"
+    if w.op == "logistic":
+        return (lambda x, o: impl.logistic_buffer(x, k, out=o)), "logistic_buffer"
+    if w.op == "gelu":
+        return (lambda x, o: impl.gelu_buffer(x, k, out=o)), "gelu_buffer"
+    return (lambda x, o: impl.softmax_rows(x, w.cols, w.temperature, k, out=o)), "softmax_rows"
+
+
+def time_cpu(fn, x, warmup: int, iters: int):
     out = np.empty_like(x)
-    kern = QUAKE2 if "quake2" in workload.kernels[0] else QUAKE
-    call = (lambda: impl.softmax_rows(x, cols, workload.temperature, kern, out=out)) \
-        if impl.kind == "reference" else \
-        (lambda: impl.softmax_rows(x, cols, workload.temperature, kern))
     for _ in range(warmup):
-        call()
+        fn(x, out)
     times = []
-    t_end = time.perf_counter() + min_seconds
-    while len(times) < max_calls and (time.perf_counter() < t_end or len(times) < 3):
+    for _ in range(iters):
         t0 = time.perf_counter()
-        call()
+        fn(x, out)
         times.append(time.perf_counter() - t0)
-    n = rows_per_call * cols
+    return times, out
+
+
+def cpu_rate_entry(n, times, **extra):
+    mean = float(np.mean(times))
+    d = {"elements_per_s": n / mean, "gbps": BYTES_PER_ELEM * n / mean / 1e9,
+         "ms_min": 1e3 * min(times), "ms_mean": 1e3 * mean, "calls": len(times)}
+    d.update(extra)
+    return d
+
+
+def cpu_configs(inputs: dict, warmup=2, iters=10, cfg5_rows=None):
+    """The reference's own CPU functions on every BASELINE config x kernel.
+    inputs: workload name -> host float32 array (the bytes the GPU consumed).
+    cfg5_rows bounds cfg5 to its first rows (single-thread runs)."""
+    from oracle.oracle import best_cpu_baseline
+    from paper_2412_00408_b200.workloads import CONFIGS
+    impl = best_cpu_baseline()
+    res = {}
+    for name, x in inputs.items():
+        w = CONFIGS[name]
+        if name == "cfg5_softmax_vocab" and cfg5_rows:
+            x = x[: cfg5_rows * w.cols]
+        for kern in w.kernels:
+            fn, api = cpu_op(impl, w, kern)
+            times, _ = time_cpu(fn, x, warmup, iters)
+            rows = x.size // w.cols
+            res[f"{name}:{kern}"] = cpu_rate_entry(
+                x.size, times, api=api,
+                sample=(f"{rows} of {w.rows} rows" if rows != w.rows else "full config"),
+                input_fingerprint=_fp(x))
     cores = impl.effective_threads() if impl.kind == "reference" else 1
-    return {"kind": impl.kind, "cores": cores, "times": times, "elements_per_call": n,
-            "value": n * len(times) / sum(times), "x": x, "kern": kern,
-            "out": out if impl.kind == "reference" else call(),
-            "sample": f"{rows_per_call} rows x {cols} cols of {workload.name} "
-                      f"(QuAKE2 softmax_rows), {len(times)} calls"}
+    return res, impl.kind, cores
 
 
-def sample_parity(qk, w, cb):
-    """The CPU baseline's sample doubles as a parity check (the oracle as the
-    checker): the GPU softmax of the same rows against the reference's output
-    from the timed calls, the restatement summed in the GPU plan's declared
-    order (bit-exact expected) and the fp64-sum restatement (2e-6 bound)."""
+def cpu_single_thread():
+    """The per-config CPU baseline again with QUAKE_THREADS=1 (the reference
+    caches its thread count at first use, parallel.cpp:23-36, hence a child
+    process; it regenerates the same bytes from the counter-based generator)."""
+    env = dict(os.environ, QUAKE_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-single-thread"],
+                             env=env, capture_output=True, text=True, timeout=300)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+
+
+def _single_thread_main():
+    from paper_2412_00408_b200.workloads import CONFIGS
+    inputs = {name: w.host() if name != "cfg5_softmax_vocab" else w.host(rows=(0, 64))
+              for name, w in CONFIGS.items()}
+    res, kind, cores = cpu_configs(inputs, warmup=1, iters=5, cfg5_rows=64)
+    print(json.dumps({"kind": kind, "cores": cores, "per_config": res}))
+    return 0
+
+
+def sample_parity(qk, w, x, ref_out, kern, rows=64):
+    """The CPU baseline doubles as a parity check (the oracle as the checker):
+    the GPU softmax of its first rows against the reference's output from the
+    timed calls, the restatement summed in the GPU plan's declared order
+    (bit-exact expected) and the fp64-sum restatement (2e-6 bound)."""
     import torch
     from oracle.oracle import Restatement
-    x, ref_out, kern = cb["x"], cb["out"], cb["kern"]
     cols = w.cols
+    x = x[: rows * cols]
+    ref_out = ref_out[: rows * cols]
     y = qk.softmax_rows(torch.from_numpy(x.ravel()).cuda(), cols,
                         qk.SoftmaxParams(temperature=w.temperature),
                         qk.KernelChoice(kern)).cpu().numpy()
@@ -204,25 +292,12 @@ def sample_parity(qk, w, cb):
     fp64sum = R.softmax_rows(x.ravel(), cols, w.temperature, kern, sum_mode=1)
     yb, ob = y.view(np.uint32), ordered.view(np.uint32)
     rel = lambda a, b: float(np.max(np.abs(a.astype(np.float64) - b) / np.abs(b)))  # noqa: E731
-    return {"sample": cb["sample"].split(",")[0],
+    return {"sample": f"first {rows} rows x {cols} cols of {w.name}",
             "mismatches_vs_ordered_restatement": int(np.count_nonzero(yb != ob)),
             "max_rel_vs_fp64_sum_restatement": rel(y, fp64sum), "tolerance": 2e-6,
             "max_rel_vs_reference_output": rel(y, np.asarray(ref_out).ravel()),
             "note": "the reference's own fp32 sequential sum drifts ~3e-4 at 128256 columns "
                     "(SURVEY F5); the 2e-6 bound is against the fp64-sum restatement"}
-
-
-def cpu_single_thread(workload_name: str):
-    """The same CPU baseline with QUAKE_THREADS=1 (the reference caches its thread
-    count at first use, parallel.cpp:23-36, hence a child process)."""
-    env = dict(os.environ, QUAKE_THREADS="1")
-    try:
-        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload",
-                              workload_name, "--cpu-rate-rows", "16"], env=env,
-                             capture_output=True, text=True, timeout=120)
-        return json.loads(out.stdout.strip().splitlines()[-1])
-    except Exception as e:  # pragma: no cover
-        return {"value": None, "error": str(e)}
 
 
 def accuracy_report(qk, w, x, y):
@@ -254,25 +329,39 @@ def accuracy_report(qk, w, x, y):
 
 
 def run_reference_arm(args):
+    """The reference's own softmax_rows (oracle/_ref: its sources compiled in
+    place) over the full cfg5 matrix, all host threads: `warmup` untimed calls,
+    then exactly `steps` timed calls (the same config and step count as our
+    arm; the rows are independent, so a call is one whole step)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    from oracle.oracle import best_cpu_baseline
     from paper_2412_00408_b200.workloads import CONFIGS
     w = CONFIGS[args.workload]
-    # each step: a bounded sample of the workload (rows) on all host threads
-    rows = args.ref_rows
-    res = cpu_reference_rate(w, rows, 0.0, args.steps, warmup=args.warmup)
-    times = res["times"]
-    value = res["value"]
+    impl = best_cpu_baseline()
+    x = w.host()
+    fn, api = cpu_op(impl, w, w.kernels[0])
+    times, _ = time_cpu(fn, x, args.warmup, args.steps)
+    n = x.size
+    value = n * len(times) / sum(times)
+    cores = impl.effective_threads() if impl.kind == "reference" else 1
+    sample = (f"{w.rows} rows x {w.cols} cols (the full {w.name} matrix) per call, "
+              f"{len(times)} timed calls after {args.warmup} warm-up calls, {api}")
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": w.name, "shape": list(w.shape), "kernel": "quake2",
-                   "temperature": w.temperature, "sample_rows_per_step": rows},
-        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": res["cores"],
-                         "kind": res["kind"], "sample": res["sample"]},
+        "config": {"workload": w.name, "shape": list(w.shape), "kernel": w.kernels[0],
+                   "temperature": w.temperature, "rows_per_step": w.rows,
+                   "input_fingerprint": {"value": _fp(x),
+                                         "algorithm": "sum of the fp32 bit patterns as int32, "
+                                                      "accumulated in int64"}},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores,
+                         "kind": impl.kind, "sample": sample,
+                         "ms_min": 1e3 * min(times), "ms_mean": 1e3 * float(np.mean(times)),
+                         **host_info()},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -290,17 +379,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg5_softmax_vocab")
-    ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--no-extras", action="store_true", help="skip per_config and cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-rate-rows", type=int, default=0,
-                    help=argparse.SUPPRESS)  # internal: print the CPU baseline rate and exit
+    ap.add_argument("--cpu-single-thread", action="store_true",
+                    help=argparse.SUPPRESS)  # internal: QUAKE_THREADS=1 child of the CPU baseline
     args = ap.parse_args()
-    if args.cpu_rate_rows:
-        from paper_2412_00408_b200.workloads import CONFIGS
-        r = cpu_reference_rate(CONFIGS[args.workload], args.cpu_rate_rows, 3.0, 40)
-        print(json.dumps({k: r[k] for k in ("kind", "cores", "value", "sample")}))
-        return 0
+    if args.cpu_single_thread:
+        return _single_thread_main()
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -313,17 +398,24 @@ def main():
     from paper_2412_00408_b200.workloads import CONFIGS
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # one GPU per rank; ranks beyond the visible GPUs share them round-robin
+    # (e.g. the 2-way split on a one-GPU box: the shards are independent)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # control plane only (barrier, max-over-ranks timing, fingerprints):
+        # there is no data-path collective, so no NCCL
+        dist.init_process_group("gloo")
     L = _lib.lib()
     # host-span calls (e2e) shard over the library's device list: this rank's GPU only
-    qk.set_devices([local])
+    qk.set_devices([dev])
     w = CONFIGS[args.workload]
     r0, r1 = row_shard(w.rows, rank, world)
     my_rows = r1 - r0
     n_local = my_rows * w.cols
-    x = w.device(rows=(r0, r1)) if world > 1 else w.device()
+    # this rank's rows of the one counter-based draw (the same bytes as rows
+    # r0..r1 of the single-GPU input)
+    x = w.device(rows=(r0, r1))
     y = torch.empty_like(x)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
@@ -338,9 +430,23 @@ def main():
             raise RuntimeError(_lib.last_error())
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def gather(v: int):
+        if world == 1:
+            return [v]
+        out = [None] * world
+        dist.all_gather_object(out, v)
+        return out
 
     # warm-up
     with torch.cuda.stream(stream):
@@ -349,10 +455,10 @@ def main():
     barrier()
     region0, region1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     try:
-        uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
     except Exception:
         uuid = None
-    with ClockSampler(local, uuid) as clk:
+    with ClockSampler(dev, uuid) as clk:
         barrier()
         clk.begin()
         # the timed region holds exactly K back-to-back launches of the kernel
@@ -378,12 +484,11 @@ def main():
     barrier()
     launch_ms = [a.elapsed_time(b) for a, b in ev]
     launch_min_ms = min(launch_ms)
-    # input fingerprint: sum of the fp32 bit patterns as int64 (stated algorithm)
-    fingerprint = int(x.view(torch.int32).sum(dtype=torch.int64).item())
-    t = torch.tensor([region_ms, float(np.mean(launch_ms))], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    region_ms, iso_ms = t.tolist()
+    # fingerprints: sum of the fp32 bit patterns as int32, in int64 (stated
+    # algorithm); per rank, so a k-way run's entries add up to the 1-GPU ones
+    in_fps = gather(int(x.view(torch.int32).sum(dtype=torch.int64).item()))
+    out_fps = gather(int(y.view(torch.int32).sum(dtype=torch.int64).item()))
+    region_ms, iso_ms = max_over_ranks([region_ms, float(np.mean(launch_ms))])
     kern_ms = region_ms / args.steps
     total_elems = w.n if world > 1 else n_local
     value = total_elems * args.steps / (region_ms * 1e-3)
@@ -402,22 +507,17 @@ def main():
     for _ in range(args.e2e_steps):
         host_call()
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = te.item()
+    e2e_s = max_over_ranks([e2e_s])[0]
     e2e_value = total_elems * args.e2e_steps / e2e_s
     assert torch.equal(hy.cuda(), y), "host-span path differs from the device path"
 
     peak, peak_kind = hbm_peak()
     achieved = BYTES_PER_ELEM * n_local / (kern_ms * 1e-3) / 1e9
     plan = qk.softmax_plan(w.cols, True, qk.KernelChoice.Quake2)
-    kernel_name = {0: "softmax_warp_vec", 1: "softmax_warp_scalar", 2: "softmax_smem",
+    kernel_name = {1: "softmax_warp_scalar", 2: "softmax_smem",
                    3: "softmax_global3", 4: "softmax_pipe (TMA pipeline, cluster)",
-                   5: "softmax_pipe_la (lookahead TMA pipeline, cluster)",
                    6: "softmax_pipe_l2 (long-row pipeline, cluster)",
                    7: "softmax_pipe_s (scalar-lane pipeline, cluster)",
-                   8: "softmax_warp_multi (short rows, several per warp)",
                    9: "softmax_thread_row (one thread per row)",
                    10: "softmax_rows_smem (one thread per row, smem tile)",
                    11: "softmax_subwarp (G lanes per row)",
@@ -429,11 +529,16 @@ def main():
         "data": "synthetic",
         "config": {"workload": w.name, "shape": list(w.shape), "kernel": "quake2",
                    "temperature": w.temperature, "rows_per_gpu": my_rows,
-                   "distribution": "N(0,4) seed 5 (torch CUDA Philox)",
+                   "distribution": "N(0,4) seed 5 (counter-based lowbias32 + Box-Muller, "
+                                   "workloads.py)",
                    "l2": "inputs (2.1 GB) larger than L2 (126 MB); no flush needed",
-                   "input_fingerprint": {"value": fingerprint,
-                                         "algorithm": "sum of this rank's fp32 bit patterns "
-                                                      "as int32, accumulated in int64"},
+                   "rows_per_rank": [list(row_shard(w.rows, r, world)) for r in range(world)],
+                   "input_fingerprint": {"value": sum(in_fps), "per_rank": in_fps,
+                                         "algorithm": "sum of the fp32 bit patterns as int32, "
+                                                      "accumulated in int64"},
+                   "output_fingerprint": {"value": sum(out_fps), "per_rank": out_fps,
+                                          "note": "same algorithm over the softmax output; "
+                                                  "equal for every GPU count"},
                    "plan": plan},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
@@ -458,17 +563,34 @@ def main():
         line["roofline"]["traffic_source"] = traffic["source"] + (
             "" if world == 1 else f", scaled to this rank's {my_rows} rows")
     if rank == 0 and world == 1 and not args.no_extras:
-        line["per_config"] = per_config(qk, L, _lib, peak)
-        try:
-            cb = cpu_reference_rate(w, 64, 8.0, 50)
-            line["cpu_baseline"] = {"value": cb["value"], "unit": "elements/s",
-                                    "cores": cb["cores"], "kind": cb["kind"],
-                                    "sample": cb["sample"]}
-            line["cpu_baseline"]["parity"] = sample_parity(qk, w, cb)
-        except Exception as e:  # pragma: no cover
-            line["cpu_baseline"] = {"value": None, "error": str(e)}
-        line["cpu_baseline"]["single_thread"] = cpu_single_thread(w.name)
         line["accuracy"] = accuracy_report(qk, w, x, y)
+        hx_np = hx.numpy()
+        del hy
+        line["per_config"], cpu_inputs = per_config(qk, L, _lib, peak)
+        try:
+            cpu_inputs[w.name] = hx_np
+            cpu, kind, cores = cpu_configs(cpu_inputs)
+            single = cpu_single_thread()
+            for key, ent in cpu.items():
+                line["per_config"].setdefault(key, {})["cpu_baseline"] = {
+                    "all_threads": dict(ent, cores=cores, kind=kind),
+                    "single_thread": dict(single.get("per_config", {}).get(key, {}),
+                                          cores=1, kind=single.get("kind"))}
+            cb = cpu[f"{w.name}:{w.kernels[0]}"]
+            line["cpu_baseline"] = {
+                "value": cb["elements_per_s"], "unit": "elements/s", "cores": cores,
+                "kind": kind, "ms_min": cb["ms_min"], "ms_mean": cb["ms_mean"],
+                "sample": f"the full {w.name} matrix ({w.rows} x {w.cols}, the bytes the GPU "
+                          f"consumed), {cb['calls']} timed calls after 2 warm-ups, "
+                          f"reference softmax_rows, all host threads",
+                "single_thread": single.get("per_config", {}).get(f"{w.name}:{w.kernels[0]}"),
+                **host_info()}
+            from oracle.oracle import QUAKE2, best_cpu_baseline
+            ref_out = best_cpu_baseline().softmax_rows(hx_np[: 64 * w.cols], w.cols,
+                                                       w.temperature, QUAKE2)
+            line["cpu_baseline"]["parity"] = sample_parity(qk, w, hx_np, ref_out, QUAKE2)
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": repr(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -541,10 +663,12 @@ def per_config(qk, L, _lib, peak, iters=12):
                 "us_isolated": iso * 1e6, "gbps_isolated": gi, "frac_isolated": gi / peak,
                 "rotation_buffers": pairs}
 
+    host_inputs = {}
     for w in (CFG1, CFG2, CFG3, CFG4):
         n = w.n
         pairs = max(2, -(-4 * l2 // (8 * n)))
         xs = [w.device() for _ in range(pairs)]
+        host_inputs[w.name] = xs[0].cpu().numpy()  # the bytes the kernels consumed
         ys = [torch.empty_like(xs[0]) for _ in range(pairs)]
         # same harness, plain device-to-device copy of the same bytes: what
         # a pure stream reaches at this size (launch + ramp overheads included)
@@ -577,7 +701,7 @@ def per_config(qk, L, _lib, peak, iters=12):
             res[f"{w.name}:{kn}"] = entry(timeit([make(x, y) for x, y in zip(xs, ys)]), n)
         del xs, ys
         torch.cuda.empty_cache()
-    return res
+    return res, host_inputs
 
 
 if __name__ == "__main__":

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define QK_ABI_VERSION 2
+#define QK_ABI_VERSION 3
 
 typedef struct CUstream_st* qk_stream; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -104,16 +104,16 @@ typedef struct {
 /* Softmax launch plan (introspection; the reduction geometry that fixes the
  * summation order, see softmax.cu). */
 typedef struct {
-  int32_t variant; /* 0 warp/float4, 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep,
-                      4 persistent TMA pipeline (+cluster), 5 its lookahead form,
+  int32_t variant; /* 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep,
+                      4 persistent TMA pipeline (+cluster),
                       6 long-row pipeline (one stage, prefix refilled early),
                       7 scalar-lane pipeline (cols % 4 != 0),
-                      8 several short rows per warp (lanes = lanes per row),
                       9 one thread per row (<= 16 cols; lanes = 1: sequential sum),
                       10 one thread per row through an smem tile (lanes = 1),
                       11 G lanes per row (lanes = G, vpt = chunks per lane),
-                      12 TMA row tiles, G lanes per row (unaligned 97-128 cols) */
-  int32_t width;   /* elements per chunk: 4 or 1 */
+                      12 TMA row tiles, G lanes per row (unaligned 33-200 cols);
+                      0, 5, 8: retired variants (numbers reserved) */
+  int32_t width;   /* elements per chunk: 4 when cols % 4 == 0, else 1 (any address) */
   int32_t lanes;   /* partial-sum lanes per CTA */
   int32_t cluster; /* CTAs per row */
   int64_t slice;   /* chunks per CTA slice (0 = whole row) */
@@ -134,9 +134,24 @@ qk_status qk_device_count(int* count);
 /* Devices the host-span operators shard over (rows / 16-byte element
  * ranges, no collectives). n = 0 restores the default (current device). */
 qk_status qk_set_devices(const int* devices, int n);
+/* As qk_set_devices, but a device may be listed several times: each entry is
+ * one shard with its own workspace and host thread. Lets one GPU run the
+ * 2/4/8-way split of the multi-GPU driver (tests; outputs do not depend on
+ * the split). */
+qk_status qk_set_device_shards(const int* devices, int n);
+/* Number of shards (entries) and their devices. */
 int qk_get_devices(int* devices, int cap);
-/* Frees cached device workspace and pinned staging used by the host-span path. */
+/* Frees the cached device workspace of the host-span path. */
 void qk_release_workspace(void);
+/* Device workspace one host-span shard may hold, in bytes (0 = automatic: 90%
+ * of free HBM). Shards whose host-side spans exceed it stream through rings
+ * of 64 MiB chunk buffers, softmax with a validation pass first. */
+void qk_set_workspace_limit(size_t bytes);
+/* Softmax planner knobs (the QK_SM_* measurement options, read from the
+ * environment once at first use): set `name` to `value`, or unset it when
+ * `clear` != 0; name = NULL clears every option. Plans are cached per
+ * (device, cols, kernel, options). QK_ERR_BAD_ARGUMENT for an unknown name. */
+qk_status qk_set_plan_override(const char* name, int32_t value, int32_t clear);
 
 /* ---- 1. coefficient derivation (kernels.cpp:25-87, nonlin.cpp:132-141) ---- */
 qk_status qk_coeffs_for(float p, float q, int32_t centering_bias, qk_affine_coeffs* out);
@@ -152,7 +167,9 @@ qk_gelu_constants qk_gelu_constants_defaults(void);
 int32_t qk_resolve_centering_bias(qk_kernel k, int32_t requested);
 const char* qk_kernel_name(qk_kernel k);
 /* Launch geometry (and hence summation order) of softmax rows of `cols`
- * columns for `kernel` on the current device. */
+ * columns for `kernel` on the current device. It depends on cols, kernel
+ * and device only: rows at any address get the same order (`aligned16` is
+ * ignored since ABI 3). */
 qk_status qk_softmax_plan(size_t cols, int32_t aligned16, qk_kernel kernel,
                           qk_softmax_plan_info* out);
 

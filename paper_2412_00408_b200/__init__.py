@@ -11,7 +11,8 @@ from .quake import (AffineCoeffs, ClampRange, GeluConstants, KernelChoice, QuadC
                     coeffs_for, default_clamp, device_count, exp_buffer, gelu, gelu_buffer,
                     get_devices, kernel_name, logistic, logistic_buffer, natural_exp_coeffs,
                     negated_natural_exp_coeffs, quake, quake2, quake2_buffer, quake_buffer,
-                    release_workspace, resolve_centering_bias, set_devices, softmax_plan,
+                    plan_override, release_workspace, resolve_centering_bias, set_device_shards,
+                    set_devices, set_plan_override, set_workspace_limit, softmax_plan,
                     softmax_row, softmax_rows)
 from ._lib import LIB_PATH, lib
 

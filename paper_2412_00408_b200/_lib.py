@@ -13,7 +13,7 @@ from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int, c_in
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 # QK_LIB_PATH: an alternative build of the same library (A/B measurements)
 LIB_PATH = os.environ.get("QK_LIB_PATH") or os.path.join(PKG_DIR, "libquake_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # qk_status
 QK_OK = 0
@@ -113,6 +113,9 @@ SIGNATURES = {
     "qk_is_invalid_argument": (c_int, [c_int]),
     "qk_device_count": (c_int, [POINTER(c_int)]),
     "qk_set_devices": (c_int, [POINTER(c_int), c_int]),
+    "qk_set_device_shards": (c_int, [POINTER(c_int), c_int]),
+    "qk_set_workspace_limit": (None, [c_size_t]),
+    "qk_set_plan_override": (c_int, [c_char_p, c_int32, c_int32]),
     "qk_get_devices": (c_int, [POINTER(c_int), c_int]),
     "qk_release_workspace": (None, []),
     "qk_coeffs_for": (c_int, [c_float, c_float, c_int32, POINTER(AffineCoeffsC)]),

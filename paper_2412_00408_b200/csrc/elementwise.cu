@@ -12,6 +12,7 @@
 // Reference paths cited relative to /root/reference/proj/.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "internal.h"
@@ -274,7 +275,46 @@ cudaError_t launch_op(const float* in, float* out, size_t n, const EwParams& p, 
   }
 }
 
+// Validation pass of the host-span softmax (nonlin.cpp:43-55 rejects any
+// non-finite element): sets bit 0 of *flags when x[0..n) holds a NaN or an
+// infinity. Reads only; used where `out` must stay untouched until every
+// row has been checked (device `out` spans, inputs larger than the
+// workspace). One flag write per CTA at most.
+__global__ void __launch_bounds__(kThreads) check_finite_kernel(const float* __restrict__ x,
+                                                                size_t n, size_t head,
+                                                                uint32_t* __restrict__ flags) {
+  pdl_entry();
+  const size_t n4 = (n - head) >> 2;
+  const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
+  bool bad = false;  // !(|v| <= FLT_MAX) holds exactly for NaN and +-Inf
+  for (size_t i = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * kThreads) {
+    const float4 v = __ldcs(x4 + i);
+    const float a = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+    // fmaxf drops a NaN operand: test NaN separately via self-comparison
+    bad |= !(a <= 3.402823466e38f) || v.x != v.x || v.y != v.y || v.z != v.z || v.w != v.w;
+  }
+  if (blockIdx.x == 0) {
+    const size_t tail0 = head + (n4 << 2);
+    if (threadIdx.x < head) bad |= !(fabsf(x[threadIdx.x]) <= 3.402823466e38f);
+    if (threadIdx.x < n - tail0) bad |= !(fabsf(x[tail0 + threadIdx.x]) <= 3.402823466e38f);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, 1u);
+}
+
 }  // namespace
+
+cudaError_t launch_check_finite(const float* x, size_t n, uint32_t* flags, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  if (reinterpret_cast<uintptr_t>(x) & 3u) return cudaErrorMisalignedAddress;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(x) & 15u;
+  const size_t head = std::min<size_t>(a == 0 ? 0 : (16u - a) / 4u, n);
+  size_t blocks = ((n - head) / 4 + kThreads * 8 - 1) / (kThreads * 8);
+  if (blocks == 0) blocks = 1;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  return launch_ex(check_finite_kernel, dim3(static_cast<unsigned>(blocks)), dim3(kThreads), 0,
+                   stream, 0, x, n, head, flags);
+}
 
 cudaError_t launch_elementwise(EwOp op, const float* in, float* out, size_t n, const EwParams& p,
                                int sm_count, cudaStream_t stream) {

@@ -5,11 +5,12 @@
 //    248-264); compiled with -ffp-contract=off like the reference build;
 //  * validation with the reference's preconditions, order and messages;
 //  * dispatch to the sm_100a kernels (elementwise.cu, softmax.cu);
-//  * the host-span path: per-device cached workspace, chunked H2D / kernel /
-//    D2H pipelines over three streams, and the multi-GPU driver that shards
-//    rows (softmax) or 16-byte-aligned element ranges (elementwise) over the
-//    configured devices with one host thread per device and no collectives
-//    — the GPU replacement of parallel_chunks (parallel.hpp:43-68).
+//  * the host-span path: per-shard cached workspace (rings of chunk buffers,
+//    or the whole shard when it fits), chunked H2D / kernel / D2H pipelines
+//    over three streams, and the multi-GPU driver that shards rows (softmax)
+//    or 16-byte-aligned element ranges (elementwise) over the configured
+//    devices with one host thread per shard and no collectives — the GPU
+//    replacement of parallel_chunks (parallel.hpp:43-68).
 // Reference paths cited relative to /root/reference/proj/.
 #include <cuda_runtime.h>
 
@@ -119,10 +120,10 @@ bool needs_x86_overflow(const qk_affine_coeffs& c, const qk_clamp_range& r) {
 }
 
 // ---------------------------------------------------------------------------
-// devices
+// devices and shards
 
 std::mutex g_dev_mu;
-std::vector<int> g_devices;  // empty = current device
+std::vector<int> g_devices;  // one entry per shard; empty = current device
 
 std::vector<int> active_devices() {
   std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -132,55 +133,113 @@ std::vector<int> active_devices() {
   return {d};
 }
 
-struct DeviceState {
-  std::mutex mu;  // serialises host-span calls on this device
-  std::atomic<int> sm_count{0};  // read lock-free by concurrent launches
-  float* d_in = nullptr;
-  float* d_out = nullptr;
-  size_t cap = 0;  // floats
-  uint32_t* d_flags = nullptr;
-  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
-};
-
-constexpr int kMaxDevices = 64;
-DeviceState g_state[kMaxDevices];
-
-int sm_count_of(int dev) {
-  DeviceState& st = g_state[dev];
-  int v = st.sm_count.load(std::memory_order_acquire);
-  if (v == 0) {
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
-      cudaGetLastError();
-      v = 148;
-    }
-    st.sm_count.store(v, std::memory_order_release);
-  }
-  return v;
-}
-
 int current_device() {
   int d = 0;
   cudaGetDevice(&d);
   return d;
 }
 
-// Caller holds st.mu and has set the device.
-qk_status ensure_workspace(DeviceState& st, size_t n) {
-  if (st.streams[0] == nullptr) {
-    for (auto& s : st.streams) QK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-    QK_CUDA(cudaMalloc(&st.d_flags, sizeof(uint32_t)), "cudaMalloc(flags)");
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sm_count[kMaxDevices];
+
+int sm_count_of(int dev) {
+  int v = dev >= 0 && dev < kMaxDevices ? g_sm_count[dev].load(std::memory_order_acquire) : 0;
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = 148;
+    }
+    if (dev >= 0 && dev < kMaxDevices) g_sm_count[dev].store(v, std::memory_order_release);
   }
-  if (n > st.cap) {
-    if (st.d_in) cudaFree(st.d_in);
-    if (st.d_out) cudaFree(st.d_out);
-    st.d_in = st.d_out = nullptr;
-    st.cap = 0;
-    const size_t want = std::max<size_t>(n, 1 << 20);
-    QK_CUDA(cudaMalloc(&st.d_in, want * sizeof(float)), "cudaMalloc(workspace in)");
-    QK_CUDA(cudaMalloc(&st.d_out, want * sizeof(float)), "cudaMalloc(workspace out)");
-    st.cap = want;
+  return v;
+}
+
+// Device workspace of one shard of the host-span path: (device, slot), slot
+// = how many earlier shards of the same call sit on that device. Buffers
+// grow on demand and are kept (qk_release_workspace frees them).
+struct Workspace {
+  std::mutex mu;  // held by the calling thread for the whole call
+  int dev = 0;
+  int slot = 0;
+  float* d_in = nullptr;
+  size_t in_cap = 0;  // floats
+  float* d_out = nullptr;
+  size_t out_cap = 0;
+  uint32_t* d_flags = nullptr;
+  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+};
+
+std::mutex g_ws_mu;
+std::vector<std::unique_ptr<Workspace>> g_ws;  // stable addresses, creation order
+std::atomic<size_t> g_ws_limit{0};             // bytes per shard; 0 = automatic
+
+Workspace* workspace_of(int dev, int slot) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (auto& w : g_ws) {
+    if (w->dev == dev && w->slot == slot) return w.get();
+  }
+  g_ws.push_back(std::make_unique<Workspace>());
+  g_ws.back()->dev = dev;
+  g_ws.back()->slot = slot;
+  return g_ws.back().get();
+}
+
+// The workspaces of one call's shards, locked in one global order (device,
+// then slot) by the calling thread and released when it returns: concurrent
+// multi-device calls cannot deadlock, and shard threads never lock.
+class ShardLease {
+ public:
+  explicit ShardLease(const std::vector<int>& devs) {
+    ws_.resize(devs.size());
+    for (size_t i = 0; i < devs.size(); ++i) {
+      int slot = 0;
+      for (size_t j = 0; j < i; ++j) slot += devs[j] == devs[i] ? 1 : 0;
+      ws_[i] = workspace_of(devs[i], slot);
+    }
+    std::vector<Workspace*> order = ws_;
+    std::sort(order.begin(), order.end(), [](const Workspace* a, const Workspace* b) {
+      return a->dev != b->dev ? a->dev < b->dev : a->slot < b->slot;
+    });
+    for (Workspace* w : order) locks_.emplace_back(w->mu);
+  }
+  Workspace& operator[](size_t i) { return *ws_[i]; }
+
+ private:
+  std::vector<Workspace*> ws_;
+  std::vector<std::unique_lock<std::mutex>> locks_;
+};
+
+// Caller holds w.mu and has set w.dev current.
+qk_status ensure_streams(Workspace& w) {
+  if (w.streams[0] == nullptr) {
+    for (auto& s : w.streams) QK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    QK_CUDA(cudaMalloc(&w.d_flags, sizeof(uint32_t)), "cudaMalloc(flags)");
   }
   return QK_OK;
+}
+
+qk_status ensure_buf(float*& p, size_t& cap, size_t n, const char* what) {
+  if (n <= cap) return QK_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  const size_t want = std::max<size_t>(n, 1 << 20);
+  QK_CUDA(cudaMalloc(&p, want * sizeof(float)), what);
+  cap = want;
+  return QK_OK;
+}
+
+// Device bytes one shard may hold in workspace: the test hook's limit, or
+// 90% of what is free plus what this workspace already holds.
+size_t workspace_budget(const Workspace& w) {
+  const size_t lim = g_ws_limit.load();
+  if (lim != 0) return lim;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (fr + (w.in_cap + w.out_cap) * sizeof(float)) / 10 * 9;
 }
 
 bool device_pointer(const void* p, int* dev) {
@@ -361,13 +420,11 @@ qk_status resolve_sm(const qk_softmax_params* prm, qk_kernel k, qk::SmKernel* sk
   return QK_OK;
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
 // ---------------------------------------------------------------------------
 // host-span drivers
 
-// Run fn(device, begin, end) for each device's shard, one host thread per
-// device beyond the first; returns the first failing status.
+// Run fn(shard, device, begin, end) for every shard, one host thread per
+// shard beyond the first; returns the first failing status.
 template <typename Fn>
 qk_status for_each_shard(const std::vector<std::pair<size_t, size_t>>& shards,
                          const std::vector<int>& devs, Fn&& fn) {
@@ -411,6 +468,7 @@ std::vector<std::pair<size_t, size_t>> make_shards(size_t n, size_t parts, size_
 }
 
 constexpr size_t kChunkElems = size_t{16} << 20;  // 64 MiB per pipeline stage
+constexpr int kRing = 3;                          // chunk buffers (= streams) per side
 
 qk_status run_elementwise_host(const EwSpec& spec, const float* xs, float* out, size_t n) {
   if (n == 0) return QK_OK;
@@ -431,34 +489,45 @@ qk_status run_elementwise_host(const EwSpec& spec, const float* xs, float* out, 
   std::vector<int> devs = in_dev ? std::vector<int>{pdev} : (out_dev ? std::vector<int>{odev}
                                                                       : active_devices());
   const auto shards = make_shards(n, devs.size(), 4);
-  return for_each_shard(shards, devs, [&](size_t, int dev, size_t b, size_t e) -> qk_status {
+  ShardLease lease(devs);
+  return for_each_shard(shards, devs, [&](size_t i, int dev, size_t b, size_t e) -> qk_status {
     const size_t len = e - b;
     if (dev < 0) return fail(QK_ERR_NO_DEVICE, "cudaSetDevice failed");
     if (len == 0) return QK_OK;
-    DeviceState& st = g_state[dev];
-    std::lock_guard<std::mutex> lk(st.mu);
-    qk_status s = ensure_workspace(st, len);
-    if (s != QK_OK) return s;
+    Workspace& w = lease[i];
+    if (qk_status s = ensure_streams(w)) return s;
+    // a ring of kRing chunk buffers per host side: chunk ci uses buffer and
+    // stream ci % kRing, so a buffer is reused only after its previous
+    // chunk's kernel and copies have retired (stream order)
+    const size_t cl_max = std::min(kChunkElems, len);
+    const size_t nbuf = std::min<size_t>(kRing, (len + cl_max - 1) / cl_max);
+    if (!in_dev) {
+      if (qk_status s = ensure_buf(w.d_in, w.in_cap, cl_max * nbuf, "cudaMalloc(workspace in)")) return s;
+    }
+    if (!out_dev) {
+      if (qk_status s = ensure_buf(w.d_out, w.out_cap, cl_max * nbuf, "cudaMalloc(workspace out)")) return s;
+    }
     const int sms = sm_count_of(dev);
     size_t ci = 0;
-    for (size_t off = 0; off < len; off += kChunkElems, ++ci) {
-      const size_t cl = std::min(kChunkElems, len - off);
-      cudaStream_t str = st.streams[ci % 3];
+    for (size_t off = 0; off < len; off += cl_max, ++ci) {
+      const size_t cl = std::min(cl_max, len - off);
+      const size_t slot = ci % nbuf;
+      cudaStream_t str = w.streams[ci % kRing];
       const float* src = xs + b + off;
-      float* dsrc = st.d_in + off;
-      if (in_dev) {
-        dsrc = const_cast<float*>(src);
-      } else {
-        QK_CUDA(cudaMemcpyAsync(dsrc, src, cl * sizeof(float), cudaMemcpyHostToDevice, str), "H2D");
+      const float* dsrc = src;
+      if (!in_dev) {
+        float* buf = w.d_in + slot * cl_max;
+        QK_CUDA(cudaMemcpyAsync(buf, src, cl * sizeof(float), cudaMemcpyHostToDevice, str), "H2D");
+        dsrc = buf;
       }
-      float* ddst = out_dev ? out + b + off : st.d_out + off;
+      float* ddst = out_dev ? out + b + off : w.d_out + slot * cl_max;
       QK_CUDA(qk::launch_elementwise(spec.op, dsrc, ddst, cl, spec.p, sms, str), "elementwise kernel");
       if (!out_dev) {
         QK_CUDA(cudaMemcpyAsync(out + b + off, ddst, cl * sizeof(float), cudaMemcpyDeviceToHost, str),
                 "D2H");
       }
     }
-    for (auto& str : st.streams) QK_CUDA(cudaStreamSynchronize(str), "stream sync");
+    for (auto& str : w.streams) QK_CUDA(cudaStreamSynchronize(str), "stream sync");
     return QK_OK;
   });
 }
@@ -485,6 +554,18 @@ qk_status validate_sm(const char* who, size_t n, size_t cols, const qk_softmax_p
   return QK_OK;
 }
 
+// softmax_rows over host or device spans (nonlin.cpp:162-189). The contract:
+// every row is validated before anything reaches `out` (nonlin.cpp:176-180),
+// across all shards. Per shard, one of two schedules:
+//  * resident — the shard's host-side spans fit the workspace budget: phase 1
+//    uploads the shard and runs the softmax into the device workspace (host
+//    `out`; the kernel's max pass raises the non-finite flag) or a
+//    validation pass (device `out`); after every shard reports clean, phase 2
+//    downloads the workspace, or runs the softmax straight into device `out`;
+//  * streamed — larger inputs: phase 1 streams the shard through a ring of
+//    chunk buffers with the validation pass only; phase 2 streams it again
+//    through H2D -> softmax -> D2H. Twice the upload, any size.
+// Device input and device output need no workspace at all.
 qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softmax_params* prm,
                            qk_kernel k, float* out) {
   qk::SmKernel sk;
@@ -503,47 +584,66 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
   std::atomic<bool> abort_all{false};
   std::barrier sync_point(static_cast<std::ptrdiff_t>(devs.size()));
   const size_t chunk_rows = std::max<size_t>(1, kChunkElems / cols);
+  ShardLease lease(devs);
 
-  s = for_each_shard(shards, devs, [&](size_t, int dev, size_t rb, size_t re) -> qk_status {
+  s = for_each_shard(shards, devs, [&](size_t i, int dev, size_t rb, size_t re) -> qk_status {
     if (dev < 0) {
       abort_all.store(true);
       sync_point.arrive_and_wait();
       return fail(QK_ERR_NO_DEVICE, "cudaSetDevice failed");
     }
-    DeviceState& st = g_state[dev];
-    std::unique_lock<std::mutex> lk(st.mu);
+    Workspace& w = lease[i];
     const size_t nrows = re - rb;
-    qk_status ss = ensure_workspace(st, nrows * cols);
-    const float* dsrc_all = in_dev ? m + rb * cols : st.d_in;
-    float* ddst_all = out_dev ? out + rb * cols : st.d_out;
-    const qk::SmPlan plan =
-        qk::plan_softmax(cols, aligned16(dsrc_all) && aligned16(ddst_all), dev, sk);
-    if (ss == QK_OK && cudaMemsetAsync(st.d_flags, 0, sizeof(uint32_t), st.streams[0]) != cudaSuccess) {
+    const qk::SmPlan plan = qk::plan_softmax(cols, dev, sk);
+    const size_t shard_elems = nrows * cols;
+    const size_t host_sides = (in_dev ? 0 : 1) + (out_dev ? 0 : 1);
+    qk_status ss = ensure_streams(w);
+    const bool resident =
+        ss == QK_OK && host_sides * shard_elems * sizeof(float) <= workspace_budget(w);
+    const size_t ring_rows = std::min(chunk_rows, std::max<size_t>(nrows, 1));
+    const size_t nbuf = std::min<size_t>(kRing, (nrows + ring_rows - 1) / std::max<size_t>(ring_rows, 1));
+    const size_t cap = resident ? shard_elems : ring_rows * cols * std::max<size_t>(nbuf, 1);
+    if (ss == QK_OK && !in_dev) ss = ensure_buf(w.d_in, w.in_cap, cap, "cudaMalloc(workspace in)");
+    if (ss == QK_OK && !out_dev && resident) ss = ensure_buf(w.d_out, w.out_cap, cap, "cudaMalloc(workspace out)");
+    if (ss == QK_OK && !out_dev && !resident) ss = ensure_buf(w.d_out, w.out_cap, cap, "cudaMalloc(workspace out)");
+    if (ss == QK_OK && cudaMemsetAsync(w.d_flags, 0, sizeof(uint32_t), w.streams[0]) != cudaSuccess) {
       ss = fail(QK_ERR_CUDA, "cudaMemset(flags)");
     }
-    if (ss == QK_OK) cudaStreamSynchronize(st.streams[0]);
-    // Phase 1: H2D + kernels (every row validated in the max pass).
+    if (ss == QK_OK) cudaStreamSynchronize(w.streams[0]);
+    // where chunk ci (rows r0..) of the input lives on the device, uploading
+    // it first when the input is host memory
+    auto stage_in = [&](size_t ci, size_t r0, size_t cr, cudaStream_t str, const float** dsrc) -> qk_status {
+      if (in_dev) {
+        *dsrc = m + (rb + r0) * cols;
+        return QK_OK;
+      }
+      float* buf = resident ? w.d_in + r0 * cols : w.d_in + (ci % nbuf) * ring_rows * cols;
+      if (cudaMemcpyAsync(buf, m + (rb + r0) * cols, cr * cols * sizeof(float),
+                          cudaMemcpyHostToDevice, str) != cudaSuccess) {
+        return fail(QK_ERR_CUDA, "H2D");
+      }
+      *dsrc = buf;
+      return QK_OK;
+    };
+    // Phase 1: upload + (softmax into the workspace | validation pass).
+    const bool compute_now = resident && !out_dev;
     size_t ci = 0;
     for (size_t r0 = 0; ss == QK_OK && r0 < nrows; r0 += chunk_rows, ++ci) {
       const size_t cr = std::min(chunk_rows, nrows - r0);
-      cudaStream_t str = st.streams[ci % 3];
-      const float* dsrc = dsrc_all + r0 * cols;
-      if (!in_dev) {
-        if (cudaMemcpyAsync(st.d_in + r0 * cols, m + (rb + r0) * cols, cr * cols * sizeof(float),
-                            cudaMemcpyHostToDevice, str) != cudaSuccess) {
-          ss = fail(QK_ERR_CUDA, "H2D");
-          break;
-        }
-      }
-      cudaError_t e = qk::launch_softmax(sk, plan, dsrc, ddst_all + r0 * cols, cr, cols, sp,
-                                         st.d_flags, str);
-      if (e != cudaSuccess) ss = cuda_fail(e, "softmax kernel");
+      cudaStream_t str = w.streams[ci % kRing];
+      const float* dsrc = nullptr;
+      ss = stage_in(ci, r0, cr, str, &dsrc);
+      if (ss != QK_OK) break;
+      cudaError_t e = compute_now ? qk::launch_softmax(sk, plan, dsrc, w.d_out + r0 * cols, cr, cols,
+                                                       sp, w.d_flags, str)
+                                  : qk::launch_check_finite(dsrc, cr * cols, w.d_flags, str);
+      if (e != cudaSuccess) ss = cuda_fail(e, compute_now ? "softmax kernel" : "validation kernel");
     }
     uint32_t flags = 0;
-    for (auto& str : st.streams) {
-      if (cudaStreamSynchronize(str) != cudaSuccess && ss == QK_OK) ss = fail(QK_ERR_CUDA, "stream sync");
+    for (auto& str : w.streams) {
+      if (str && cudaStreamSynchronize(str) != cudaSuccess && ss == QK_OK) ss = fail(QK_ERR_CUDA, "stream sync");
     }
-    if (ss == QK_OK && cudaMemcpy(&flags, st.d_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
+    if (ss == QK_OK && cudaMemcpy(&flags, w.d_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
                            cudaSuccess) {
       ss = fail(QK_ERR_CUDA, "D2H(flags)");
     }
@@ -554,17 +654,32 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
     if (ss != QK_OK) return ss;
     if (non_finite.load()) return fail(QK_ERR_NON_FINITE, "softmax: non-finite input");
     if (abort_all.load()) return fail(QK_ERR_CUDA, "softmax: aborted (another device failed)");
-    if (!out_dev) {
-      ci = 0;
-      for (size_t r0 = 0; r0 < nrows; r0 += chunk_rows, ++ci) {
-        const size_t cr = std::min(chunk_rows, nrows - r0);
-        QK_CUDA(cudaMemcpyAsync(out + (rb + r0) * cols, st.d_out + r0 * cols,
-                                cr * cols * sizeof(float), cudaMemcpyDeviceToHost,
-                                st.streams[ci % 3]),
+    // Phase 2: write back (download the workspace | softmax into out | stream).
+    ci = 0;
+    for (size_t r0 = 0; r0 < nrows; r0 += chunk_rows, ++ci) {
+      const size_t cr = std::min(chunk_rows, nrows - r0);
+      cudaStream_t str = w.streams[ci % kRing];
+      float* hdst = out + (rb + r0) * cols;
+      if (compute_now) {
+        QK_CUDA(cudaMemcpyAsync(hdst, w.d_out + r0 * cols, cr * cols * sizeof(float),
+                                cudaMemcpyDeviceToHost, str),
+                "D2H");
+        continue;
+      }
+      const float* dsrc = nullptr;
+      if (resident) {
+        dsrc = in_dev ? m + (rb + r0) * cols : w.d_in + r0 * cols;  // uploaded in phase 1
+      } else if (qk_status st2 = stage_in(ci, r0, cr, str, &dsrc)) {
+        return st2;
+      }
+      float* ddst = out_dev ? hdst : w.d_out + (ci % nbuf) * ring_rows * cols;
+      QK_CUDA(qk::launch_softmax(sk, plan, dsrc, ddst, cr, cols, sp, nullptr, str), "softmax kernel");
+      if (!out_dev) {
+        QK_CUDA(cudaMemcpyAsync(hdst, ddst, cr * cols * sizeof(float), cudaMemcpyDeviceToHost, str),
                 "D2H");
       }
-      for (auto& str : st.streams) QK_CUDA(cudaStreamSynchronize(str), "stream sync");
     }
+    for (auto& str : w.streams) QK_CUDA(cudaStreamSynchronize(str), "stream sync");
     return QK_OK;
   });
   if (non_finite.load() && (s == QK_OK || s == QK_ERR_NON_FINITE)) {
@@ -596,22 +711,33 @@ qk_status qk_device_count(int* count) {
   return QK_OK;
 }
 
-qk_status qk_set_devices(const int* devices, int n) {
+namespace {
+qk_status set_device_list(const int* devices, int n, bool allow_repeat, const char* who) {
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+  if (n > 0 && devices == nullptr) return fail(QK_ERR_BAD_ARGUMENT, std::string(who) + ": null pointer");
   std::vector<int> v;
   for (int i = 0; i < n; ++i) {
     if (devices[i] < 0 || devices[i] >= count || devices[i] >= kMaxDevices) {
-      return fail(QK_ERR_NO_DEVICE, "set_devices: no such device");
+      return fail(QK_ERR_NO_DEVICE, std::string(who) + ": no such device");
     }
-    if (std::find(v.begin(), v.end(), devices[i]) != v.end()) {
-      return fail(QK_ERR_BAD_ARGUMENT, "set_devices: duplicate device");
+    if (!allow_repeat && std::find(v.begin(), v.end(), devices[i]) != v.end()) {
+      return fail(QK_ERR_BAD_ARGUMENT, std::string(who) + ": duplicate device");
     }
     v.push_back(devices[i]);
   }
   std::lock_guard<std::mutex> lk(g_dev_mu);
   g_devices = v;
   return QK_OK;
+}
+}  // namespace
+
+qk_status qk_set_devices(const int* devices, int n) {
+  return set_device_list(devices, n, false, "set_devices");
+}
+
+qk_status qk_set_device_shards(const int* devices, int n) {
+  return set_device_list(devices, n, true, "set_device_shards");
 }
 
 int qk_get_devices(int* devices, int cap) {
@@ -620,23 +746,34 @@ int qk_get_devices(int* devices, int cap) {
   return static_cast<int>(v.size());
 }
 
+void qk_set_workspace_limit(size_t bytes) { g_ws_limit.store(bytes); }
+
+qk_status qk_set_plan_override(const char* name, int32_t value, int32_t clear) {
+  if (!qk::set_plan_opt(name, value, clear != 0)) {
+    return fail(QK_ERR_BAD_ARGUMENT, std::string("set_plan_override: unknown option ") +
+                                         (name ? name : "(null)"));
+  }
+  return QK_OK;
+}
+
 void qk_release_workspace(void) {
   int prev = current_device();
-  for (int d = 0; d < kMaxDevices; ++d) {
-    DeviceState& st = g_state[d];
-    std::lock_guard<std::mutex> lk(st.mu);
-    if (st.streams[0] == nullptr && st.d_in == nullptr) continue;
-    cudaSetDevice(d);
-    if (st.d_in) cudaFree(st.d_in);
-    if (st.d_out) cudaFree(st.d_out);
-    if (st.d_flags) cudaFree(st.d_flags);
-    for (auto& s : st.streams) {
-      if (s) cudaStreamDestroy(s);
-      s = nullptr;
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  for (auto& wp : g_ws) {
+    Workspace& w = *wp;
+    std::lock_guard<std::mutex> lk(w.mu);
+    if (w.streams[0] == nullptr && w.d_in == nullptr && w.d_out == nullptr) continue;
+    cudaSetDevice(w.dev);
+    if (w.d_in) cudaFree(w.d_in);
+    if (w.d_out) cudaFree(w.d_out);
+    if (w.d_flags) cudaFree(w.d_flags);
+    for (auto& st : w.streams) {
+      if (st) cudaStreamDestroy(st);
+      st = nullptr;
     }
-    st.d_in = st.d_out = nullptr;
-    st.d_flags = nullptr;
-    st.cap = 0;
+    w.d_in = w.d_out = nullptr;
+    w.d_flags = nullptr;
+    w.in_cap = w.out_cap = 0;
   }
   cudaSetDevice(prev);
 }
@@ -685,14 +822,14 @@ const char* qk_kernel_name(qk_kernel k) {
   }
   return "unknown";
 }
-qk_status qk_softmax_plan(size_t cols, int32_t aligned, qk_kernel kernel,
+qk_status qk_softmax_plan(size_t cols, int32_t /*aligned16: ignored since ABI 3*/, qk_kernel kernel,
                           qk_softmax_plan_info* out) {
   if (!out) return fail(QK_ERR_BAD_ARGUMENT, "softmax_plan: null pointer");
   qk::SmKernel sk;
   qk::SmParams sp;
   qk_softmax_params prm{1.0f, -1, {1.0f / 3.0f, 0.0f, 2.0f / 3.0f}};
   if (qk_status s = resolve_sm(&prm, kernel, &sk, &sp)) return s;
-  const qk::SmPlan p = qk::plan_softmax(cols, aligned != 0, current_device(), sk);
+  const qk::SmPlan p = qk::plan_softmax(cols, current_device(), sk);
   out->variant = static_cast<int32_t>(p.variant);
   out->width = p.width;
   out->lanes = p.lanes;
@@ -873,8 +1010,10 @@ qk_status qk_softmax_rows_device(const float* matrix, size_t n, size_t cols,
   if (s != QK_OK) return s;
   const size_t rows = n / cols;
   LaunchDevice on(stream, matrix);
-  const qk::SmPlan plan =
-      qk::plan_softmax(cols, aligned16(matrix) && aligned16(out), current_device(), sk);
+  if ((reinterpret_cast<uintptr_t>(matrix) | reinterpret_cast<uintptr_t>(out)) & 3u) {
+    return fail(QK_ERR_BAD_ARGUMENT, "softmax_rows: pointer not aligned to a float");
+  }
+  const qk::SmPlan plan = qk::plan_softmax(cols, current_device(), sk);
   const cudaError_t e = qk::launch_softmax(sk, plan, matrix, out, rows, cols, sp, d_flags,
                                            reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? QK_OK : cuda_fail(e, "softmax kernel launch");

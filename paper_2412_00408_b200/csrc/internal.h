@@ -47,6 +47,9 @@ struct EwParams {
 cudaError_t launch_elementwise(EwOp op, const float* in, float* out, size_t n,
                                const EwParams& p, int sm_count, cudaStream_t stream);
 
+// Validation pass: OR 1 into *flags (device) when x[0..n) holds a non-finite value.
+cudaError_t launch_check_finite(const float* x, size_t n, uint32_t* flags, cudaStream_t stream);
+
 // ---- row softmax ----
 
 enum class SmKernel : int { kExact = 0, kQuake = 1, kQuake2 = 2, kQuake2General = 3,
@@ -58,15 +61,15 @@ enum class SmKernel : int { kExact = 0, kQuake = 1, kQuake2 = 2, kQuake2General 
 // Reduction geometry of one launch (also reported through qk_softmax_plan so
 // the tests can restate the exact summation order).
 enum class SmVariant : int {
-  kWarpVec = 0,     // warp per row, row in registers, float4 lanes
+  // 0 (warp per row, float4 lanes), 5 (two-row lookahead pipeline) and 8
+  // (several short rows per warp): retired, measured slower than the kernels
+  // below; the numbers stay reserved
   kWarpScalar = 1,  // warp per row, row in registers, scalar lanes
   kSmem = 2,        // CTA (or cluster of CTAs) per row, row staged in smem
   kGlobal3 = 3,     // CTA per row, three sweeps over global memory (huge rows)
   kPipe = 4,        // persistent cluster per row group, multi-stage TMA pipeline
-  kPipeLA = 5,      // kPipe with the cluster exchange awaited one row late
   kPipeL2 = 6,      // long rows: one smem stage, prefix refilled under the exps
   kPipeS = 7,       // kPipe with one-float chunks: rows of cols % 4 != 0 (unaligned)
-  kWarpMulti = 8,   // 32/G short rows per warp, G lanes each (order of kWarpVec/kWarpScalar)
   kThreadRow = 9,   // one thread per row (<= 16 cols): the reference's sequential order
   kRowsSmem = 10,   // one thread per row, rows staged through smem (coalesced), <= 64 cols
   kSubWarp = 11,    // G lanes per aligned row, up to 8 float4 chunks each (lanes = G)
@@ -85,6 +88,8 @@ struct SmPlan {
   int stages;       // kPipe: row slices in flight per CTA
   int balanced;     // kPipe: rank r owns q (+1 if r < nchunks % cluster) chunks
   int resident;     // kPipe: clusters resident at once (occupancy API; 0 = unknown)
+  int rr;           // kWarpScalar: rows per warp (1 or 2)
+  int pf;           // kPipeL2: rows bulk-prefetched into L2 ahead (0 = off)
 };
 
 struct SmParams {
@@ -97,10 +102,20 @@ struct SmParams {
   float nat_c0, nat_c1, nat_lo, nat_hi;  // unfused kinds: natural-exp coefficients / clamp
   int unfused;      // 1: kQuakeUnfused / kQuake2Unfused
   int pdl_late;     // persistent kernels: trigger the dependent launch after the last row
+  // 16-byte phase of every row's input / output in floats (0..3). Nonzero only
+  // for float4-chunk plans (cols % 4 == 0) on a base that is not 16-byte
+  // aligned; the kernels then read straddling chunks and split the stores,
+  // keeping the chunk order, so results do not depend on the address.
+  int iph, oph;
 };
 
-// The plan depends on the kernel kind's arithmetic weight (see softmax.cu).
-SmPlan plan_softmax(size_t cols, bool aligned16, int device, SmKernel kind);
+// The plan depends on (device, cols, kind) and the planner options only —
+// never on the row count or the data's address (see softmax.cu). Cached.
+SmPlan plan_softmax(size_t cols, int device, SmKernel kind);
+// Planner options (QK_SM_* measurement knobs): environment read once, then
+// qk_set_plan_override. set_plan_opt(nullptr, ...) clears all; false = unknown name.
+int plan_opt(const char* name, int dflt);
+bool set_plan_opt(const char* name, int value, bool clear);
 
 // Launch softmax over `rows` rows of `cols` columns. `flags` (device, may be
 // null) receives bit 0 when a non-finite input was seen.
@@ -173,5 +188,9 @@ int pipe_resident_probe(int variant, int cluster, int threads, size_t smem);
 cudaError_t launch_softmax(SmKernel k, const SmPlan& plan, const float* in, float* out,
                            size_t rows, size_t cols, const SmParams& p, uint32_t* flags,
                            cudaStream_t stream);
+// launch_softmax with p.iph / p.oph already set
+cudaError_t launch_softmax_phased(SmKernel k, const SmPlan& plan, const float* in, float* out,
+                                  size_t rows, size_t cols, const SmParams& p, uint32_t* flags,
+                                  cudaStream_t stream);
 
 }  // namespace qk

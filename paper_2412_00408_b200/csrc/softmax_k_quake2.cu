@@ -10,7 +10,7 @@ cudaError_t launch_softmax_quake2(const SmPlan& plan, const float* in, float* ou
 }
 
 // Clusters of the persistent pipelines resident at once for one launch shape
-// (the planner's occupancy probe; variant 4 = kPipe, 5 = kPipeLA, 6 = kPipeL2, 7 = kPipeS).
+// (the planner's occupancy probe; variant 4 = kPipe, 6 = kPipeL2, 7 = kPipeS).
 int pipe_resident_probe(int variant, int cluster, int threads, size_t smem) {
   if (variant == 7) {
     return resident_clusters(softmax_pipe_s<SmKernel::kQuake2, 40>, cluster, threads, smem);
@@ -18,9 +18,7 @@ int pipe_resident_probe(int variant, int cluster, int threads, size_t smem) {
   if (variant == 6) {
     return resident_clusters(softmax_pipe_l2<SmKernel::kQuake2, 16>, cluster, threads, smem);
   }
-  return variant == 5 ? resident_clusters(softmax_pipe_la<SmKernel::kQuake2, 8>, cluster, threads, smem)
-                      : resident_clusters(softmax_pipe<SmKernel::kQuake2, true, 16>, cluster, threads,
-                                          smem);
+  return resident_clusters(softmax_pipe<SmKernel::kQuake2, true, 16>, cluster, threads, smem);
 }
 
 }  // namespace qk

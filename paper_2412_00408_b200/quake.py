@@ -196,7 +196,9 @@ def clamp_for(c: AffineCoeffs) -> ClampRange:
 def softmax_plan(cols: int, aligned16: bool = True,
                  kernel: "KernelChoice" = None) -> dict:
     """Launch geometry the library picks for rows of `cols` columns and the
-    given kernel choice (default Quake2); it fixes the summation order."""
+    given kernel choice (default Quake2); it fixes the summation order. It
+    depends on `cols`, the kernel and the device only, never on the data's
+    address (`aligned16` is accepted for compatibility and ignored)."""
     p = SoftmaxPlanC()
     k = KernelChoice.Quake2 if kernel is None else kernel
     _check(_lib.lib().qk_softmax_plan(cols, int(aligned16), int(k), ctypes.byref(p)))
@@ -216,6 +218,44 @@ def set_devices(devices) -> None:
     devs = list(devices or [])
     arr = (ctypes.c_int * max(1, len(devs)))(*devs)
     _check(_lib.lib().qk_set_devices(arr, len(devs)))
+
+
+def set_device_shards(devices) -> None:
+    """Like set_devices, but a device may repeat: one shard (own workspace,
+    own host thread) per entry — runs the multi-GPU split on one GPU."""
+    devs = list(devices or [])
+    arr = (ctypes.c_int * max(1, len(devs)))(*devs)
+    _check(_lib.lib().qk_set_device_shards(arr, len(devs)))
+
+
+def set_workspace_limit(nbytes: int) -> None:
+    """Device workspace per host-span shard in bytes (0 = automatic). Larger
+    host inputs stream through chunk rings (softmax: validation pass first)."""
+    _lib.lib().qk_set_workspace_limit(int(nbytes))
+
+
+def set_plan_override(name: Optional[str], value: int = 0, clear: bool = False) -> None:
+    """Set (or with ``clear`` unset) a softmax planner knob (QK_SM_*); name
+    None clears all. The environment is read once, at first use."""
+    _check(_lib.lib().qk_set_plan_override(None if name is None else name.encode(),
+                                           int(value), int(bool(clear))))
+
+
+class plan_override:
+    """Context manager: ``with plan_override(QK_SM_TILES=1): ...``."""
+
+    def __init__(self, **opts):
+        self.opts = opts
+
+    def __enter__(self):
+        for k, v in self.opts.items():
+            set_plan_override(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k in self.opts:
+            set_plan_override(k, 0, clear=True)
+        return False
 
 
 def get_devices() -> list:
@@ -280,6 +320,25 @@ def _dev_tensor(x, writable=False):
     return x
 
 
+def _mixed_spans(xs, out):
+    """Pointers and sizes for a host-span call where at most one side may be a
+    CUDA tensor. The converted tensors/arrays are returned in ``keep`` so they
+    outlive the C call, and torch's current stream is synchronised AFTER the
+    conversions: the library's host-span path runs on its own streams, so any
+    pending producer (or the conversion itself) must have finished."""
+    hx = _Host(xs) if not _is_cuda_tensor(xs) else None
+    ho = _Host(out, writable=True) if not _is_cuda_tensor(out) else None
+    dx = None if hx else _dev_tensor(xs)
+    do = None if ho else _dev_tensor(out, True)
+    xp, n = (hx.ptr, hx.size) if hx else (dx.data_ptr(), dx.numel())
+    op, on = (ho.ptr, ho.size) if ho else (do.data_ptr(), do.numel())
+    if dx is not None or do is not None:
+        import torch
+        dev = (dx if dx is not None else do).device
+        torch.cuda.current_stream(dev).synchronize()
+    return xp, n, op, on, (hx, ho, dx, do)
+
+
 def _run_elementwise(xs, out, host_fn, dev_fn):
     """host_fn(xp, n, op, on) / dev_fn(xp, op, n, stream) -> status."""
     if out is None:
@@ -291,14 +350,9 @@ def _run_elementwise(xs, out, host_fn, dev_fn):
             raise QuakeInvalidArgument(1, "output size mismatch")
         _check(dev_fn(x.data_ptr(), o.data_ptr(), x.numel(), _stream_handle()))
         return out
-    hx = _Host(xs) if not _is_cuda_tensor(xs) else None
-    ho = _Host(out, writable=True) if not _is_cuda_tensor(out) else None
-    xp, n = (hx.ptr, hx.size) if hx else (_dev_tensor(xs).data_ptr(), xs.numel())
-    op, on = (ho.ptr, ho.size) if ho else (_dev_tensor(out, True).data_ptr(), out.numel())
-    if _is_cuda_tensor(xs) or _is_cuda_tensor(out):
-        import torch
-        torch.cuda.current_stream().synchronize()
+    xp, n, op, on, keep = _mixed_spans(xs, out)
     _check(host_fn(xp, n, op, on))
+    del keep
     return out
 
 
@@ -441,11 +495,9 @@ def softmax_rows(matrix, cols: int, params: Optional[SoftmaxParams] = None,
         if check and int(flags.item()) & 1:
             raise QuakeInvalidArgument(5, "softmax: non-finite input")
         return out
-    hx = _Host(matrix) if not _is_cuda_tensor(matrix) else None
-    ho = _Host(out, writable=True) if not _is_cuda_tensor(out) else None
-    xp, n = (hx.ptr, hx.size) if hx else (_dev_tensor(matrix).data_ptr(), matrix.numel())
-    op, on = (ho.ptr, ho.size) if ho else (_dev_tensor(out, True).data_ptr(), out.numel())
+    xp, n, op, on, keep = _mixed_spans(matrix, out)
     _check(L.qk_softmax_rows(xp, n, cols, ctypes.byref(pc), int(kernel), op, on))
+    del keep
     return out
 
 
@@ -457,12 +509,7 @@ def softmax_row(v, params: Optional[SoftmaxParams] = None,
     pc = params._c()
     if out is None:
         out = _new_like(v)
-    hx = _Host(v) if not _is_cuda_tensor(v) else None
-    ho = _Host(out, writable=True) if not _is_cuda_tensor(out) else None
-    if _is_cuda_tensor(v) or _is_cuda_tensor(out):
-        import torch
-        torch.cuda.current_stream().synchronize()
-    xp, n = (hx.ptr, hx.size) if hx else (_dev_tensor(v).data_ptr(), v.numel())
-    op, on = (ho.ptr, ho.size) if ho else (_dev_tensor(out, True).data_ptr(), out.numel())
+    xp, n, op, on, keep = _mixed_spans(v, out)
     _check(L.qk_softmax_row(xp, n, ctypes.byref(pc), int(kernel), op, on))
+    del keep
     return out

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _run(env_extra):
     env = dict(os.environ, **env_extra)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--steps", "2", "--warmup", "1", "--ref-rows", "4"],
+                          "--steps", "2", "--warmup", "1"],
                          capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     return [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
@@ -31,7 +31,9 @@ def test_reference_arm_json_contract():
     assert d["higher_is_better"] is True and d["config"]["workload"] == "cfg5_softmax_vocab"
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] == d["value"]
-    assert "rows" in cb["sample"]
+    assert "4096 rows x 128256 cols" in cb["sample"] and "2 timed calls" in cb["sample"]
+    assert cb["ms_min"] <= cb["ms_mean"] and cb["nproc"] >= 1 and cb["arch"]
+    assert d["config"]["rows_per_step"] == 4096
     e2e = d["e2e"]
     assert e2e["value"] == d["value"] and e2e["unit"] == d["unit"]
     assert e2e["h2d_bytes_per_step"] == 0 and e2e["d2h_bytes_per_step"] == 0

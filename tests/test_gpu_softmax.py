@@ -112,18 +112,45 @@ def test_general_quad_and_bias_overrides():
                             f"bias={bias} k={kern}")
 
 
-def test_misaligned_rows_use_scalar_variants():
+@pytest.mark.parametrize("cols", [4, 6, 8, 12, 16, 20, 64, 512, 517, 1024, 1028, 1152, 4096, 5000,
+                                  16384, 128256, 262144, 1 << 20])
+def test_results_do_not_depend_on_the_address(cols):
+    """The reference's output does not depend on where the buffers sit; neither
+    does ours: the plan depends on cols only, and rows whose base is not 16-byte
+    aligned (every row shares the phase when cols % 4 == 0) run the same chunk
+    order with straddling loads and split stores. Input and output offsets of
+    0-3 floats, independently: bit-identical to the aligned run and to the
+    ordered restatement. Covers every float4 family: thread per row, sub-warp,
+    staged smem (1028), two-stage and long-row pipelines, global sweeps (2^20)."""
     R = restatement()
-    for cols in (6, 517, 5000):
-        rows = 16
-        base = (np.random.default_rng(cols).standard_normal(rows * cols + 1) * 2).astype(np.float32)
-        xd = torch.from_numpy(base).cuda()[1:]  # 4-byte offset: not 16-byte aligned
-        out = torch.empty(rows * cols + 1, device="cuda")[1:]
-        qk.softmax_rows(xd, cols, qk.SoftmaxParams(), K.Quake2, out=out)
-        plan = qk.softmax_plan(cols, False, K.Quake2)
-        assert plan["width"] == 1
-        assert_bitexact(out.cpu().numpy(), R.softmax_rows_ordered(base[1:], cols, plan, 1.0,
-                                                                  QUAKE2), f"cols={cols}")
+    rows = max(2, min(40, (1 << 22) // cols))
+    n = rows * cols
+    rng = np.random.default_rng(cols + 5)
+    base = (rng.standard_normal(n + 4) * 3).astype(np.float32)
+    if n >= 8 * cols:
+        base[1 + 3 * cols: 1 + 4 * cols] = rng.uniform(-1e30, 1e30, cols)  # x86 row (offset 1)
+    xd_all = torch.from_numpy(base).cuda()
+    out_all = torch.empty(n + 4, device="cuda")
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, True, K(kern))
+        assert plan["width"] == (4 if cols % 4 == 0 else 1), plan
+        ref = None
+        for io, oo in ((0, 0), (1, 1), (2, 3), (3, 0), (0, 2), (1, 0)):
+            xd = xd_all[io: io + n]
+            out = out_all[oo: oo + n]
+            out.fill_(7.0)
+            qk.softmax_rows(xd, cols, qk.SoftmaxParams(temperature=0.5), K(kern), out=out)
+            y = out.cpu().numpy().copy()
+            if ref is None or io != 0:
+                want = R.softmax_rows_ordered(base[io: io + n], cols, plan, 0.5, kern)
+                assert_bitexact(y, want, f"cols={cols} k={kern} in+{io} out+{oo} plan={plan}")
+            if io == 0:
+                ref = y if ref is None else ref
+                assert_bitexact(y, ref, f"cols={cols} k={kern} out offset {oo}")
+        # neighbours of the written span are untouched
+        out_all.fill_(7.0)
+        qk.softmax_rows(xd_all[1: 1 + n], cols, qk.SoftmaxParams(), K(kern), out=out_all[1: 1 + n])
+        assert out_all[0].item() == 7.0 and out_all[n + 1].item() == 7.0
 
 
 @pytest.mark.parametrize("cols", [64, 63, 1001, 50257])
@@ -241,20 +268,6 @@ def test_large_host_path_validates_every_row_before_writeback():
     assert_bitexact(y2, y, "after a rejected call")
 
 
-@pytest.mark.parametrize("cols", [16384, 128256])
-def test_lookahead_variant_keeps_the_order(cols, monkeypatch):
-    """The experimental two-row-lookahead schedule (kPipeLA, QK_SM_LA=1) sums in the
-    same declared order: bit-exact against the ordered restatement of its plan."""
-    monkeypatch.setenv("QK_SM_LA", "1")
-    R = restatement()
-    plan = qk.softmax_plan(cols, True, K.Quake2)
-    assert plan["variant"] == 5
-    rows = 40
-    x = (np.random.default_rng(cols + 7).standard_normal(rows * cols) * 4).astype(np.float32)
-    y = _gpu_softmax(x, cols, 1.0, QUAKE2)
-    assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"LA cols={cols}")
-
-
 @pytest.mark.parametrize("cols", [202048, 262144, 300000])
 def test_long_row_pipeline_is_default_and_bitexact(cols):
     """Long vocab rows take the one-stage long-row pipeline (kPipeL2) and keep the
@@ -272,11 +285,10 @@ def test_long_row_pipeline_is_default_and_bitexact(cols):
 
 
 @pytest.mark.parametrize("cols,pf", [(16384, "0"), (128256, "0"), (128256, "2"), (50000, "1")])
-def test_long_row_pipeline_forced_keeps_the_order(cols, pf, monkeypatch):
+def test_long_row_pipeline_forced_keeps_the_order(cols, pf, plan_opts):
     """kPipeL2 forced (QK_SM_L2=1) on shorter rows, with and without L2 bulk
     prefetch: both kernel kinds, both temperatures, bit-exact."""
-    monkeypatch.setenv("QK_SM_L2", "1")
-    monkeypatch.setenv("QK_SM_PF", pf)
+    plan_opts(QK_SM_L2=1, QK_SM_PF=int(pf))
     R = restatement()
     for kern in (QUAKE, QUAKE2):
         plan = qk.softmax_plan(cols, True, K(kern))
@@ -289,7 +301,7 @@ def test_long_row_pipeline_forced_keeps_the_order(cols, pf, monkeypatch):
                             f"forced L2 cols={cols} k={kern} t={t} pf={pf}")
 
 
-def test_long_row_pipeline_extreme_and_non_finite_rows(monkeypatch):
+def test_long_row_pipeline_extreme_and_non_finite_rows():
     """kPipeL2 rows on the x86-emulation path (huge magnitudes) and the clamp path
     stay bit-exact; a non-finite value in any row raises the flag."""
     R = restatement()
@@ -313,10 +325,10 @@ def test_long_row_pipeline_extreme_and_non_finite_rows(monkeypatch):
 
 @pytest.mark.parametrize("cols", [1, 2, 3, 4, 5, 7, 8, 12, 15, 16, 17, 24, 31, 32, 33, 48, 63, 64,
                                   65])
-def test_short_rows_several_per_warp(cols):
-    """Rows of <= 16 chunks run 32/G rows per warp (kWarpMulti) with the warp-per-row
-    order: bit-exact against the ordered restatement, with a row count that leaves
-    dead lanes in the last warp, and x86-emulated (huge-magnitude), clamped and
+def test_short_rows_mixed_paths(cols):
+    """Short rows (one thread per row, smem-staged rows, sub-warp lanes, row tiles):
+    bit-exact against the ordered restatement, with a row count that leaves dead
+    lanes in the last warp, and x86-emulated (huge-magnitude), clamped and
     ordinary rows interleaved so neighbouring rows in one warp take different paths."""
     R = restatement()
     rng = np.random.default_rng(cols + 100)
@@ -347,11 +359,11 @@ def test_short_rows_several_per_warp(cols):
 
 
 @pytest.mark.parametrize("cols", [1, 3, 8, 17, 31, 32, 33, 48, 63, 64])
-def test_rows_staged_in_smem_sequential_order(cols, monkeypatch):
+def test_rows_staged_in_smem_sequential_order(cols, plan_opts):
     """kRowsSmem (one thread per row, rows staged through shared memory) keeps the
     reference's sequential order: bit-exact against the reference-order restatement
     for a row count that ends in a partial CTA, with x86 and clamped rows mixed in."""
-    monkeypatch.setenv("QK_SM_ROWSMEM", "1")
+    plan_opts(QK_SM_ROWSMEM=1)
     R = restatement()
     rng = np.random.default_rng(cols + 7)
     rows = 700
@@ -369,11 +381,11 @@ def test_rows_staged_in_smem_sequential_order(cols, monkeypatch):
 
 
 @pytest.mark.parametrize("cols", [20, 32, 64, 100, 128, 256, 512, 1000, 1024])
-def test_subwarp_rows_keep_the_declared_order(cols, monkeypatch):
+def test_subwarp_rows_keep_the_declared_order(cols, plan_opts):
     """kSubWarp (G lanes per aligned row, chunks l, l+G, ... per lane; QK_SM_SUBWARP=1):
     bit-exact against the ordered restatement of its plan, x86 and clamped rows
     interleaved, a partial last warp."""
-    monkeypatch.setenv("QK_SM_SUBWARP", "1")
+    plan_opts(QK_SM_SUBWARP=1)
     R = restatement()
     rng = np.random.default_rng(cols + 31)
     rows = 509
@@ -390,35 +402,13 @@ def test_subwarp_rows_keep_the_declared_order(cols, monkeypatch):
                             f"subwarp cols={cols} k={kern} t={t} plan={plan}")
 
 
-@pytest.mark.parametrize("cols", [49, 77, 197, 257, 513, 577, 1001, 1023])
-def test_subwarp_scalar_rows_keep_the_declared_order(cols, monkeypatch):
-    """Scalar-lane sub-warp rows (G lanes per unaligned row; default for 49-96
-    columns, forced up to 1024 with QK_SM_SUBWARP_S=1):
-    bit-exact against the ordered restatement, x86 and clamped rows interleaved."""
-    monkeypatch.setenv("QK_SM_SUBWARP_S", "1")
-    R = restatement()
-    rng = np.random.default_rng(cols + 41)
-    rows = 389
-    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
-    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
-    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
-    x = x.ravel()
-    for kern in (QUAKE, QUAKE2):
-        plan = qk.softmax_plan(cols, False, K(kern))
-        assert plan["variant"] == 11 and plan["width"] == 1, plan
-        for t in (0.125, 1.0):
-            y = _gpu_softmax(x, cols, t, kern)
-            assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, t, kern),
-                            f"subwarp-s cols={cols} k={kern} t={t} plan={plan}")
-
-
 @pytest.mark.parametrize("cols", [97, 127, 129, 161, 197, 257, 513, 577, 1001, 1023])
 @pytest.mark.parametrize("rows", [1, 37, 389])
-def test_row_tiles_keep_the_declared_order(cols, rows, monkeypatch):
+def test_row_tiles_keep_the_declared_order(cols, rows, plan_opts):
     """kTiles (TMA row tiles through smem for unaligned rows, G lanes per row;
     default for 97-200 columns, forced up to 1024 with QK_SM_TILES=1): bit-exact against the ordered restatement with full tiles, a
     partial last tile and a single row; x86 and clamped rows interleaved."""
-    monkeypatch.setenv("QK_SM_TILES", "1")
+    plan_opts(QK_SM_TILES=1)
     R = restatement()
     rng = np.random.default_rng(cols * 7 + rows)
     x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
