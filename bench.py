@@ -576,6 +576,10 @@ def main():
                     "all_threads": dict(ent, cores=cores, kind=kind),
                     "single_thread": dict(single.get("per_config", {}).get(key, {}),
                                           cores=1, kind=single.get("kind"))}
+            line["per_config"][f"{w.name}:{w.kernels[0]}"].update({
+                "us": kern_ms * 1e3, "elements_per_s": n_local / (kern_ms * 1e-3),
+                "gbps": achieved, "frac": achieved / peak, "us_isolated": iso_ms * 1e3,
+                "note": "GPU numbers: the headline timed region above"})
             cb = cpu[f"{w.name}:{w.kernels[0]}"]
             line["cpu_baseline"] = {
                 "value": cb["elements_per_s"], "unit": "elements/s", "cores": cores,
