@@ -96,6 +96,11 @@ typedef struct {
   qk_quad_coeffs quad;
 } qk_softmax_params;
 
+/* bitcore.hpp:32-53 FpFormat (layout of a binary floating-point format) */
+typedef struct {
+  int32_t exponent_bits, mantissa_bits, bias;
+} qk_fp_format;
+
 /* nonlin.hpp:55-62 GeluConstants */
 typedef struct {
   float kappa, root2_over_pi, fused_scale, inverse_kappa;
@@ -159,6 +164,11 @@ qk_affine_coeffs qk_natural_exp_coeffs(int32_t centering_bias);
 qk_affine_coeffs qk_base2_coeffs(int32_t centering_bias);
 qk_affine_coeffs qk_negated_natural_exp_coeffs(int32_t centering_bias);
 qk_status qk_default_clamp(float p, float q, qk_clamp_range* out);
+/* kernels.cpp:25-40 / :74-82 with an explicit format (kernels.hpp:50-51, 89):
+ * scale 2^mantissa_bits, exponent bias `bias`. NULL = binary32. */
+qk_status qk_coeffs_for_format(float p, float q, const qk_fp_format* fmt, int32_t centering_bias,
+                               qk_affine_coeffs* out);
+qk_status qk_default_clamp_format(float p, float q, const qk_fp_format* fmt, qk_clamp_range* out);
 qk_clamp_range qk_clamp_for(const qk_affine_coeffs* c);
 qk_quad_coeffs qk_quad_continuity(void);
 qk_quad_coeffs qk_quad_minimax(void);
@@ -198,6 +208,16 @@ qk_status qk_softmax_row(const float* v, size_t n, const qk_softmax_params* para
  * = expf, QK_FAST_EXP = __expf, QK_QUAKE/QK_QUAKE2 = natural-exp QuAKE with
  * the per-kernel default bias. */
 qk_status qk_exp_buffer(const float* xs, size_t n, float* out, size_t out_n, qk_kernel k);
+
+/* Scalar forms: kernels.hpp:141-155 quake / quake2, nonlin.cpp:198-208
+ * logistic, nonlin.cpp:277-290 gelu. One element through the same GPU
+ * kernels (a per-thread pinned mailbox and one small launch on the first
+ * configured device); bit-identical to the buffer forms. */
+qk_status qk_quake(float x, const qk_affine_coeffs* c, const qk_clamp_range* r, float* y);
+qk_status qk_quake2(float x, const qk_affine_coeffs* c, const qk_quad_coeffs* a,
+                    const qk_clamp_range* r, float* y);
+qk_status qk_logistic(float x, qk_kernel k, int32_t centering_bias, float* y);
+qk_status qk_gelu(float x, qk_kernel k, int32_t centering_bias, float* y);
 
 /* ---- 3. device operators (stream-ordered, device pointers, no sync) ---- */
 qk_status qk_quake_buffer_device(const float* xs, float* out, size_t n,

@@ -61,22 +61,25 @@ qk_status cuda_fail(cudaError_t e, const char* where) {
 // ---------------------------------------------------------------------------
 // coefficient derivation
 
-qk_affine_coeffs make_coeffs(float p, float q, bool bias) {
+qk_affine_coeffs make_coeffs(float p, float q, bool bias, int mantissa_bits = 23,
+                             int exp_bias = 127) {
   // kernels.cpp:30-39
+  const double scale = std::ldexp(1.0, mantissa_bits);
   const double beta = bias ? kCenteringBias : 0.0;
   qk_affine_coeffs c;
-  c.c0 = static_cast<float>(kScale * static_cast<double>(p));
-  c.c1 = static_cast<float>(kScale * (static_cast<double>(127) + static_cast<double>(q) - beta));
+  c.c0 = static_cast<float>(scale * static_cast<double>(p));
+  c.c1 = static_cast<float>(scale * (static_cast<double>(exp_bias) + static_cast<double>(q) - beta));
   c.input_scale = p;
   c.input_shift = q;
   c.bias_applied = bias ? 1 : 0;
   return c;
 }
 
-qk_clamp_range solve_clamp(double c0, double c1) {
+qk_clamp_range solve_clamp(double c0, double c1, int mantissa_bits = 23) {
   // kernels.cpp:64-70
-  double a = (kLowExponentEdge * kScale - c1) / c0;
-  double b = (kHighExponentEdge * kScale - c1) / c0;
+  const double scale = std::ldexp(1.0, mantissa_bits);
+  double a = (kLowExponentEdge * scale - c1) / c0;
+  double b = (kHighExponentEdge * scale - c1) / c0;
   if (a > b) std::swap(a, b);
   return {static_cast<float>(a), static_cast<float>(b)};
 }
@@ -800,6 +803,25 @@ qk_status qk_default_clamp(float p, float q, qk_clamp_range* out) {
                      kScale * (static_cast<double>(127) + static_cast<double>(q)));
   return QK_OK;
 }
+qk_status qk_coeffs_for_format(float p, float q, const qk_fp_format* fmt, int32_t bias,
+                               qk_affine_coeffs* out) {
+  if (!out) return fail(QK_ERR_BAD_ARGUMENT, "coeffs_for: null pointer");
+  if (p == 0.0f) return fail(QK_ERR_ZERO_SLOPE, "coeffs_for: input scale p must be non-zero");
+  *out = fmt ? make_coeffs(p, q, bias != 0, fmt->mantissa_bits, fmt->bias)
+             : make_coeffs(p, q, bias != 0);
+  return QK_OK;
+}
+qk_status qk_default_clamp_format(float p, float q, const qk_fp_format* fmt, qk_clamp_range* out) {
+  if (!out) return fail(QK_ERR_BAD_ARGUMENT, "default_clamp: null pointer");
+  if (p == 0.0f) return fail(QK_ERR_ZERO_SLOPE, "default_clamp: input scale p must be non-zero");
+  // kernels.cpp:74-82
+  const int mb = fmt ? fmt->mantissa_bits : 23;
+  const int eb = fmt ? fmt->bias : 127;
+  const double scale = std::ldexp(1.0, mb);
+  *out = solve_clamp(scale * static_cast<double>(p),
+                     scale * (static_cast<double>(eb) + static_cast<double>(q)), mb);
+  return QK_OK;
+}
 qk_clamp_range qk_clamp_for(const qk_affine_coeffs* c) {
   return solve_clamp(static_cast<double>(c->c0), static_cast<double>(c->c1));
 }
@@ -908,6 +930,81 @@ qk_status qk_softmax_row(const float* v, size_t n, const qk_softmax_params* prm,
   if (s != QK_OK) return s;
   if (!v || !out) return fail(QK_ERR_BAD_ARGUMENT, "softmax_row: null pointer");
   return run_softmax_host(v, n, n, prm, k, out);
+}
+
+// ---- scalar forms ----
+namespace {
+// Per-thread pinned mailbox {x, y} (mapped: the kernel reads x and writes y
+// in host memory) and a stream, on the first configured device.
+struct ScalarBox {
+  int dev = -1;
+  float* h = nullptr;
+  cudaStream_t s = nullptr;
+  ~ScalarBox() {
+    if (h) cudaFreeHost(h);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+thread_local ScalarBox t_box;
+
+qk_status run_scalar(const EwSpec& spec, float x, float* y) {
+  if (!y) return fail(QK_ERR_BAD_ARGUMENT, "scalar form: null output pointer");
+  const int dev = active_devices()[0];
+  const int prev = current_device();
+  if (dev != prev) QK_CUDA(cudaSetDevice(dev), "cudaSetDevice");
+  struct Restore {
+    int prev, dev;
+    ~Restore() {
+      if (prev != dev) cudaSetDevice(prev);
+    }
+  } restore{prev, dev};
+  if (t_box.dev != dev) {
+    if (t_box.h) cudaFreeHost(t_box.h);
+    if (t_box.s) cudaStreamDestroy(t_box.s);
+    t_box.h = nullptr;
+    t_box.s = nullptr;
+    t_box.dev = -1;
+    QK_CUDA(cudaHostAlloc(&t_box.h, 8 * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable),
+            "cudaHostAlloc(scalar)");
+    QK_CUDA(cudaStreamCreateWithFlags(&t_box.s, cudaStreamNonBlocking), "cudaStreamCreate");
+    t_box.dev = dev;
+  }
+  float* d = nullptr;
+  QK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), t_box.h, 0),
+          "cudaHostGetDevicePointer");
+  volatile float* h = t_box.h;
+  h[0] = x;
+  // x and y 16 bytes apart: both float4-aligned, one element each
+  QK_CUDA(qk::launch_elementwise(spec.op, d, d + 4, 1, spec.p, sm_count_of(dev), t_box.s),
+          "elementwise kernel");
+  QK_CUDA(cudaStreamSynchronize(t_box.s), "stream sync");
+  *y = h[4];
+  return QK_OK;
+}
+}  // namespace
+
+qk_status qk_quake(float x, const qk_affine_coeffs* c, const qk_clamp_range* r, float* y) {
+  if (!c || !r) return fail(QK_ERR_BAD_ARGUMENT, "quake: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kQuake, QK_QUAKE, -1, c, r, nullptr, &spec);
+  return s != QK_OK ? s : run_scalar(spec, x, y);
+}
+qk_status qk_quake2(float x, const qk_affine_coeffs* c, const qk_quad_coeffs* a,
+                    const qk_clamp_range* r, float* y) {
+  if (!c || !r || !a) return fail(QK_ERR_BAD_ARGUMENT, "quake2: null pointer");
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kQuake2, QK_QUAKE2, -1, c, r, a, &spec);
+  return s != QK_OK ? s : run_scalar(spec, x, y);
+}
+qk_status qk_logistic(float x, qk_kernel k, int32_t bias, float* y) {
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kLogistic, k, bias, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : run_scalar(spec, x, y);
+}
+qk_status qk_gelu(float x, qk_kernel k, int32_t bias, float* y) {
+  EwSpec spec;
+  qk_status s = resolve_ew(Family::kGelu, k, bias, nullptr, nullptr, nullptr, &spec);
+  return s != QK_OK ? s : run_scalar(spec, x, y);
 }
 
 // ---- device operators ----
