@@ -6,9 +6,9 @@ Python face of that ABI, mirroring the reference's ``quake::`` operator API
 (see :mod:`.quake`). There is no CPU fallback: every operator fails loudly if
 the library is missing.
 """
-from .quake import (AffineCoeffs, ClampRange, GeluConstants, KernelChoice, QuadCoeffs,
+from .quake import (AffineCoeffs, ClampRange, FpFormat, GeluConstants, KernelChoice, QuadCoeffs,
                     QuakeCudaError, QuakeInvalidArgument, SoftmaxParams, base2_coeffs, clamp_for,
-                    coeffs_for, default_clamp, device_count, exp_buffer, gelu, gelu_buffer,
+                    coeffs_for, default_clamp, kSingle, device_count, exp_buffer, gelu, gelu_buffer,
                     get_devices, kernel_name, logistic, logistic_buffer, natural_exp_coeffs,
                     negated_natural_exp_coeffs, quake, quake2, quake2_buffer, quake_buffer,
                     plan_override, release_workspace, resolve_centering_bias, set_device_shards,

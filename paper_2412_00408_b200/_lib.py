@@ -45,6 +45,10 @@ class SoftmaxParamsC(Structure):
     _fields_ = [("temperature", c_float), ("centering_bias", c_int32), ("quad", QuadCoeffsC)]
 
 
+class FpFormatC(Structure):
+    _fields_ = [("exponent_bits", c_int32), ("mantissa_bits", c_int32), ("bias", c_int32)]
+
+
 class GeluConstantsC(Structure):
     _fields_ = [("kappa", c_float), ("root2_over_pi", c_float), ("fused_scale", c_float),
                 ("inverse_kappa", c_float)]
@@ -123,6 +127,15 @@ SIGNATURES = {
     "qk_base2_coeffs": (AffineCoeffsC, [c_int32]),
     "qk_negated_natural_exp_coeffs": (AffineCoeffsC, [c_int32]),
     "qk_default_clamp": (c_int, [c_float, c_float, POINTER(ClampRangeC)]),
+    "qk_coeffs_for_format": (c_int, [c_float, c_float, POINTER(FpFormatC), c_int32,
+                                     POINTER(AffineCoeffsC)]),
+    "qk_default_clamp_format": (c_int, [c_float, c_float, POINTER(FpFormatC),
+                                        POINTER(ClampRangeC)]),
+    "qk_quake": (c_int, [c_float, POINTER(AffineCoeffsC), POINTER(ClampRangeC), _fp]),
+    "qk_quake2": (c_int, [c_float, POINTER(AffineCoeffsC), POINTER(QuadCoeffsC),
+                          POINTER(ClampRangeC), _fp]),
+    "qk_logistic": (c_int, [c_float, c_int, c_int32, _fp]),
+    "qk_gelu": (c_int, [c_float, c_int, c_int32, _fp]),
     "qk_clamp_for": (ClampRangeC, [POINTER(AffineCoeffsC)]),
     "qk_quad_continuity": (QuadCoeffsC, []),
     "qk_quad_minimax": (QuadCoeffsC, []),

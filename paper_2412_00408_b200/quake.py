@@ -163,9 +163,37 @@ class SoftmaxParams:
 
 # ---- coefficient derivation (kernels.cpp:25-87) ----
 
-def coeffs_for(p: float, q: float = 0.0, centering_bias: bool = False) -> AffineCoeffs:
+@dataclass(frozen=True)
+class FpFormat:
+    """bitcore.hpp:32-53: exponent width, mantissa width, exponent bias."""
+    exponent_bits: int = 8
+    mantissa_bits: int = 23
+    bias: int = 127
+
+    @staticmethod
+    def single() -> "FpFormat":
+        return FpFormat(8, 23, 127)
+
+    def _c(self):
+        return _lib.FpFormatC(self.exponent_bits, self.mantissa_bits, self.bias)
+
+
+kSingle = FpFormat.single()
+
+
+def coeffs_for(p: float, q: float = 0.0, *args, centering_bias: bool = False,
+               fmt: Optional[FpFormat] = None) -> AffineCoeffs:
+    """kernels.cpp:25-40. Positional forms: (p, q, centering_bias) or the
+    reference's (p, q, fmt, centering_bias)."""
+    args = list(args)
+    if args and isinstance(args[0], FpFormat):
+        fmt = args.pop(0)
+    if args:
+        centering_bias = args.pop(0)
     out = AffineCoeffsC()
-    _check(_lib.lib().qk_coeffs_for(p, q, int(bool(centering_bias)), ctypes.byref(out)))
+    f = (fmt or kSingle)._c()
+    _check(_lib.lib().qk_coeffs_for_format(p, q, ctypes.byref(f), int(bool(centering_bias)),
+                                           ctypes.byref(out)))
     return AffineCoeffs._from(out)
 
 
@@ -182,9 +210,11 @@ def negated_natural_exp_coeffs(centering_bias: bool = True) -> AffineCoeffs:
         _lib.lib().qk_negated_natural_exp_coeffs(int(bool(centering_bias))))
 
 
-def default_clamp(p: float, q: float = 0.0) -> ClampRange:
+def default_clamp(p: float, q: float = 0.0, fmt: Optional[FpFormat] = None) -> ClampRange:
+    """kernels.cpp:74-82."""
     out = ClampRangeC()
-    _check(_lib.lib().qk_default_clamp(p, q, ctypes.byref(out)))
+    f = (fmt or kSingle)._c()
+    _check(_lib.lib().qk_default_clamp_format(p, q, ctypes.byref(f), ctypes.byref(out)))
     return ClampRange(F32(out.lo), F32(out.hi))
 
 
@@ -393,17 +423,23 @@ def quake2_buffer(xs, *args, out=None):
 
 
 def quake(x: float, c: AffineCoeffs, r: Optional[ClampRange] = None) -> np.float32:
-    """kernels.hpp:141-143 / kernels.cpp:92 — evaluated on the GPU."""
+    """kernels.hpp:141-143 / kernels.cpp:92 — evaluated on the GPU (qk_quake)."""
     r = clamp_for(c) if r is None else r
-    return quake_buffer(np.array([x], dtype=np.float32), c, r)[0]
+    y = ctypes.c_float()
+    _check(_lib.lib().qk_quake(float(x), ctypes.byref(c._c()), ctypes.byref(r._c()),
+                               ctypes.byref(y)))
+    return np.float32(y.value)
 
 
 def quake2(x: float, c: AffineCoeffs, a: Optional[QuadCoeffs] = None,
            r: Optional[ClampRange] = None) -> np.float32:
-    """kernels.hpp:146-155 / kernels.cpp:94-96 — evaluated on the GPU."""
+    """kernels.hpp:146-155 / kernels.cpp:94-96 — evaluated on the GPU (qk_quake2)."""
     a = QuadCoeffs.continuity() if a is None else a
     r = clamp_for(c) if r is None else r
-    return quake2_buffer(np.array([x], dtype=np.float32), c, a, r)[0]
+    y = ctypes.c_float()
+    _check(_lib.lib().qk_quake2(float(x), ctypes.byref(c._c()), ctypes.byref(a._c()),
+                                ctypes.byref(r._c()), ctypes.byref(y)))
+    return np.float32(y.value)
 
 
 # ---- nonlin.hpp:83-97 ----
@@ -456,14 +492,19 @@ def exp_buffer(xs, kernel: KernelChoice, out=None):
 
 
 def logistic(x: float, kernel: KernelChoice, centering_bias: Optional[bool] = None) -> np.float32:
-    """nonlin.cpp:198-208 — evaluated on the GPU."""
-    return logistic_buffer(np.array([x], dtype=np.float32), KernelChoice(kernel),
-                           centering_bias)[0]
+    """nonlin.cpp:198-208 — evaluated on the GPU (qk_logistic)."""
+    y = ctypes.c_float()
+    _check(_lib.lib().qk_logistic(float(x), int(KernelChoice(kernel)), _bias_arg(centering_bias),
+                                  ctypes.byref(y)))
+    return np.float32(y.value)
 
 
 def gelu(x: float, kernel: KernelChoice, centering_bias: Optional[bool] = None) -> np.float32:
-    """nonlin.cpp:277-290 — evaluated on the GPU."""
-    return gelu_buffer(np.array([x], dtype=np.float32), KernelChoice(kernel), centering_bias)[0]
+    """nonlin.cpp:277-290 — evaluated on the GPU (qk_gelu)."""
+    y = ctypes.c_float()
+    _check(_lib.lib().qk_gelu(float(x), int(KernelChoice(kernel)), _bias_arg(centering_bias),
+                              ctypes.byref(y)))
+    return np.float32(y.value)
 
 
 # ---- nonlin.hpp:70-81 ----

@@ -199,3 +199,31 @@ def test_kernel_names_and_unfused_bias_resolution():
     assert qk.resolve_centering_bias(K.QuakeUnfused, None) is True
     assert qk.resolve_centering_bias(K.Quake2Unfused, None) is False
     assert qk.resolve_centering_bias(K.Quake2Unfused, True) is True
+
+
+def test_coeffs_for_takes_the_reference_format_argument():
+    """kernels.hpp:50-51, 89: coeffs_for(p, q, fmt = kSingle, bias) and
+    default_clamp(p, q, fmt = kSingle); the derivation follows fmt's mantissa
+    width and exponent bias (kernels.cpp:30-39, 74-82), computed in binary64."""
+    import math
+    import struct
+
+    def f32(v):
+        return struct.unpack("<f", struct.pack("<f", v))[0]
+
+    p = f32(math.log2(math.e))
+    a = qk.coeffs_for(p, 0.0, qk.kSingle, True)
+    b = qk.coeffs_for(p, 0.0, True)
+    assert (a.c0, a.c1) == (b.c0, b.c1) == (f32(2.0**23 * p), f32(2.0**23 * (127 - 0.0436)))
+    half = qk.FpFormat(5, 10, 15)
+    h = qk.coeffs_for(0.7, 0.25, half, False)
+    assert h.c0 == f32(1024.0 * f32(0.7)) and h.c1 == f32(1024.0 * (15 + 0.25))
+    r = qk.default_clamp(1.0, 0.0, half)
+    lo = (1.01 * 1024 - 1024 * 15) / 1024.0
+    hi = (254.99 * 1024 - 1024 * 15) / 1024.0
+    assert (r.lo, r.hi) == (f32(lo), f32(hi))
+    assert qk.default_clamp(1.0, 0.0) == qk.default_clamp(1.0, 0.0, qk.kSingle)
+    with pytest.raises(ValueError, match="input scale p must be non-zero"):
+        qk.coeffs_for(0.0, 1.0, half)
+    with pytest.raises(ValueError, match="input scale p must be non-zero"):
+        qk.default_clamp(0.0, 0.0, half)
