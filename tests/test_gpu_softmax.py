@@ -11,6 +11,8 @@ Two bars per case:
     rounding, ~3e-4).
 Reference tests mirrored: tests/test_nonlin.cpp:42-204, acceptance.cpp:178-254.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -69,8 +71,10 @@ def test_cfg4_full_size():
 
 @pytest.mark.slow
 def test_cfg5_rows_and_full_properties():
-    """cfg5 [4096,128256] N(0,4) QuAKE2: 64 rows bit-exact + fp64-sum tolerance; the full
-    matrix through size-independent properties (normalisation, row independence)."""
+    """cfg5 [4096,128256] N(0,4) QuAKE2, every row: bit-exact against the
+    restatement in the plan's declared order and within 2e-6 of the fp64-sum
+    restatement (row blocks checked on all host cores); the full matrix also
+    through size-independent properties (normalisation, row independence)."""
     R = restatement()
     cols = CFG5.cols
     xd = CFG5.device()
@@ -78,14 +82,27 @@ def test_cfg5_rows_and_full_properties():
     y = qk.softmax_rows(xd, cols, p, K.Quake2)
     torch.cuda.synchronize()
     plan = qk.softmax_plan(cols, True, K.Quake2)
-    sub = slice(0, 64 * cols)
-    xs = xd[sub].cpu().numpy()
-    ys = y[sub].cpu().numpy()
-    assert_bitexact(ys, R.softmax_rows_ordered(xs, cols, plan, 1.0, QUAKE2), "cfg5 rows 0..63")
-    assert max_rel(ys, R.softmax_rows(xs, cols, 1.0, QUAKE2, sum_mode=1)) <= TOL
+    xs_all = xd.cpu().numpy()
+    ys_all = y.cpu().numpy()
+
+    def check(r0, r1):
+        sub = slice(r0 * cols, r1 * cols)
+        xs, ys = xs_all[sub], ys_all[sub]
+        assert_bitexact(ys, R.softmax_rows_ordered(xs, cols, plan, 1.0, QUAKE2),
+                        f"cfg5 rows {r0}..{r1 - 1}")
+        return max_rel(ys, R.softmax_rows(xs, cols, 1.0, QUAKE2, sum_mode=1))
+
+    from concurrent.futures import ThreadPoolExecutor
+    blocks = [(r0, min(CFG5.rows, r0 + 64)) for r0 in range(0, CFG5.rows, 64)]
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        rels = list(ex.map(lambda b: check(*b), blocks))
+    assert max(rels) <= TOL, max(rels)
     # reported, not bounded: the reference's own fp32 sequential-sum rounding
+    xs, ys = xs_all[: 64 * cols], ys_all[: 64 * cols]
     dev_ref = max_rel(ys, R.softmax_rows(xs, cols, 1.0, QUAKE2, sum_mode=0))
-    print(f"cfg5 deviation from the reference's sequential fp32 sum: {dev_ref:.3e}")
+    print(f"cfg5: all {CFG5.rows} rows bit-exact (ordered), max rel vs fp64 sum {max(rels):.3e}; "
+          f"deviation from the reference's sequential fp32 sum: {dev_ref:.3e}")
+    del xs_all, ys_all
     # full matrix: rows sum to 1 within 4N ulp (acceptance.cpp:225-254), all positive
     ym = y.view(CFG5.rows, cols).double()
     sums = ym.sum(dim=1)

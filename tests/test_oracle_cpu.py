@@ -152,6 +152,28 @@ def test_restatement_matches_compiled_reference_random_bits():
             assert_bitexact(R.gelu_buffer(x, k, b), F.gelu_buffer(x, k, b))
 
 
+@pytest.mark.slow
+@pytest.mark.skipif(reference() is None, reason="reference not compiled here")
+def test_restatement_matches_compiled_reference_strided_exhaustive():
+    """Every 64th binary32 bit pattern (2^26 inputs, all exponents, signs, NaN
+    and infinity classes) for the six exhaustively GPU-swept variants:
+    restatement == compiled reference. (The GPU sweep itself compares every
+    one of the 2^32 patterns against the reference directly.)"""
+    R, F = restatement(), reference()
+    x = (np.arange(0, 1 << 26, dtype=np.uint64) * 64 + 37).astype(np.uint32).view(np.float32)
+    for bias, quad_kernel in ((1, QUAKE), (0, QUAKE2)):
+        c0, c1 = F.named_coeffs("natural", bias == 1)
+        lo, hi = F.clamp_for(c0, c1)
+        if quad_kernel == QUAKE:
+            assert_bitexact(R.quake_buffer(x, c0, c1, lo, hi), F.quake_buffer(x, c0, c1, lo, hi))
+        else:
+            assert_bitexact(R.quake2_buffer(x, c0, c1, CONTINUITY, lo, hi),
+                            F.quake2_buffer(x, c0, c1, CONTINUITY, lo, hi))
+    for k in (QUAKE, QUAKE2):
+        assert_bitexact(R.logistic_buffer(x, k), F.logistic_buffer(x, k))
+        assert_bitexact(R.gelu_buffer(x, k), F.gelu_buffer(x, k))
+
+
 @pytest.mark.skipif(reference() is None, reason="reference not compiled here")
 def test_restatement_matches_compiled_reference_softmax():
     R, F = restatement(), reference()
