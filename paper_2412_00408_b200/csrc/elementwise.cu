@@ -100,8 +100,10 @@ __device__ __forceinline__ float apply(float x, const EwParams& p) {
 
 // Two elements of the QuAKE ops with the paired FMUL2/FFMA2 sequences of
 // numerics.cuh (bit-identical to apply<OP>); other ops go element-wise.
+// `ok` is cleared when a lane left the range where the paired fast division
+// equals the IEEE one; the caller then recomputes those elements with apply.
 template <EwOp OP, bool X86>
-__device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p) {
+__device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p, bool& ok) {
   if constexpr (X86 || !(OP == EwOp::kQuake || OP == EwOp::kQuake2 ||
                          OP == EwOp::kQuake2General || OP == EwOp::kLogisticQuake ||
                          OP == EwOp::kLogisticQuake2 || OP == EwOp::kGeluQuake ||
@@ -144,10 +146,7 @@ __device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p) {
     } else {
       quake2_body2<false>(u0, u1, p.c0, p.c1, 0.f, 0.f, 0.f, e0, e1);
     }
-    const float y0 = __fdiv_rn(a, __fadd_rn(1.0f, e0));
-    const float y1 = __fdiv_rn(b, __fadd_rn(1.0f, e1));
-    a = y0 != y0 ? x86_quiet(a) : y0;
-    b = y1 != y1 ? x86_quiet(b) : y1;
+    div2_ge1(a, b, __fadd_rn(1.0f, e0), __fadd_rn(1.0f, e1), ok);
   } else {
     const float u0 = saturate_fast(a, p.lo, p.hi), u1 = saturate_fast(b, p.lo, p.hi);
     float e0, e1;
@@ -159,8 +158,7 @@ __device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p) {
       quake2_body2<false>(u0, u1, p.c0, p.c1, 0.f, 0.f, 0.f, e0, e1);
     }
     if constexpr (OP == EwOp::kLogisticQuake || OP == EwOp::kLogisticQuake2) {
-      a = __frcp_rn(__fadd_rn(1.0f, e0));
-      b = __frcp_rn(__fadd_rn(1.0f, e1));
+      recip2_ge1(__fadd_rn(1.0f, e0), __fadd_rn(1.0f, e1), a, b, ok);
     } else {
       a = e0;
       b = e1;
@@ -169,10 +167,24 @@ __device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p) {
 }
 
 template <EwOp OP, bool X86>
-__device__ __forceinline__ float4 apply4(float4 v, const EwParams& p) {
-  apply2<OP, X86>(v.x, v.y, p);
-  apply2<OP, X86>(v.z, v.w, p);
+__device__ __forceinline__ float4 apply4(float4 v, const EwParams& p, bool& ok) {
+  apply2<OP, X86>(v.x, v.y, p, ok);
+  apply2<OP, X86>(v.z, v.w, p, ok);
   return v;
+}
+
+// The exact element-wise path (IEEE divisions), for float4s the fast path refused.
+template <EwOp OP, bool X86>
+__device__ __forceinline__ float4 apply4_exact(float4 v, const EwParams& p) {
+  return make_float4(apply<OP, X86>(v.x, p), apply<OP, X86>(v.y, p), apply<OP, X86>(v.z, p),
+                     apply<OP, X86>(v.w, p));
+}
+
+template <EwOp OP, bool X86>
+__device__ __forceinline__ float4 apply4_checked(float4 v, const EwParams& p) {
+  bool ok = true;
+  const float4 y = apply4<OP, X86>(v, p, ok);
+  return __builtin_expect(ok, 1) ? y : apply4_exact<OP, X86>(v, p);
 }
 
 // Vector path: in+head and out+head are both 16-byte aligned. Each CTA
@@ -199,7 +211,7 @@ __global__ void __launch_bounds__(kThreads) ew_vec_kernel(const float* __restric
       for (int u = 0; u < U; ++u) v[u] = __ldcs(in4 + base + u * kThreads + threadIdx.x);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        __stcs(out4 + base + u * kThreads + threadIdx.x, apply4<OP, X86>(v[u], p));
+        __stcs(out4 + base + u * kThreads + threadIdx.x, apply4_checked<OP, X86>(v[u], p));
       }
     } else {
 #pragma unroll
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(kThreads) ew_vec_kernel(const float* __restric
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const size_t i = base + u * kThreads + threadIdx.x;
-        if (i < n4) __stcs(out4 + i, apply4<OP, X86>(v[u], p));
+        if (i < n4) __stcs(out4 + i, apply4_checked<OP, X86>(v[u], p));
       }
     }
   }
