@@ -12,9 +12,10 @@ import torch  # noqa: E402
 import paper_2412_00408_b200 as qk  # noqa: E402
 from paper_2412_00408_b200 import _lib  # noqa: E402
 
-NAMES = {0: "warp_vec", 1: "warp_scalar", 2: "smem", 3: "global3", 4: "pipe", 5: "pipe_la",
-         6: "pipe_l2", 7: "pipe_s", 8: "warp_multi", 9: "thread_row", 10: "rows_smem",
-         11: "subwarp", 12: "tiles"}
+NAMES = {1: "warp_scalar", 2: "smem", 3: "global3", 4: "pipe", 6: "pipe_l2", 7: "pipe_s",
+         9: "thread_row", 10: "rows_smem", 11: "subwarp", 12: "tiles"}
+# IOFF / OOFF: input / output offsets in floats (0-3) from a 16-byte boundary
+IOFF, OOFF = int(os.environ.get("IOFF", "0")), int(os.environ.get("OOFF", "0"))
 L = _lib.lib()
 stream = torch.cuda.Stream()
 sh = stream.cuda_stream
@@ -22,8 +23,9 @@ prm = qk.SoftmaxParams(temperature=1.0)._c()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"]
 total = 4096 * 128256
-x = torch.randn(total, device="cuda") * 4
-y = torch.empty_like(x)
+xb = torch.randn(total + 4, device="cuda") * 4
+yb = torch.empty_like(xb)
+x, y = xb[IOFF:IOFF + total], yb[OOFF:OOFF + total]
 cols_list = [int(c) for c in os.environ.get("COLS", "4,7,16,31,32,64,77,127,128,197,256,257,512,"
                                             "577,1001,1024,2047,4096,4097,16384,50000,50257,"
                                             "128256,151936,151937,202048,256000,262144").split(",")]
@@ -48,6 +50,7 @@ for cols in cols_list:
     torch.cuda.synchronize()
     us = a.elapsed_time(b) * 1e3 / 10
     gbs = 8 * n / us / 1e3
-    print(json.dumps({"cols": cols, "aligned": cols % 4 == 0, "kernel": NAMES[plan["variant"]],
+    print(json.dumps({"cols": cols, "aligned": cols % 4 == 0, "ioff": IOFF, "ooff": OOFF,
+                      "kernel": NAMES[plan["variant"]],
                       "lanes": plan["lanes"], "cluster": plan["cluster"], "us": round(us, 1),
                       "gbps": round(gbs, 1), "frac": round(gbs / peak, 3)}), flush=True)

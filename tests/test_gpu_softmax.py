@@ -36,7 +36,7 @@ def _gpu_softmax(x, cols, t, kernel, bias=None, quad=None):
     return y.cpu().numpy()
 
 
-@pytest.mark.parametrize("cols", [1, 2, 3, 5, 31, 32, 33, 100, 127, 128, 129, 511, 512, 513,
+@pytest.mark.parametrize("cols", [1, 2, 3, 5, 31, 32, 33, 100, 127, 128, 129, 511, 512, 513, 1028, 1100, 1536,
                                   1000, 1024, 1025, 2048, 3001, 4096, 16384, 16387, 50000,
                                   128256, 131072, 300000])
 @pytest.mark.parametrize("kernel", [QUAKE, QUAKE2])
