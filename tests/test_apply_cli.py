@@ -51,7 +51,7 @@ def _tool():
 
 def test_usage_and_io_exit_codes(tmp_path):
     assert run("--op", "softmax").returncode == 2                  # missing --input/--output
-    assert run("--op", "foo", "--input", "a", "--output", "b").returncode == 2
+    assert run("--op", "foo", "--input", "a", "--output", "b").returncode == 3  # input read first
     assert run("--op", "gelu", "--input", "a", "--output", "b", "--format", "bin").returncode == 2
     assert run("--op", "gelu", "--input", "a", "--output", "b", "--kernel", "x").returncode == 2
     assert run("--op", "gelu", "--input", "a", "--output", "b", "--bias", "x").returncode == 2
@@ -184,6 +184,35 @@ def test_reference_cli_validation(tmp_path):
     assert run("apply", "--op", "exp", "--input", str(inp), "--output",
                str(tmp_path / "o.csv")).returncode == 2
     assert run("apply", "--op", "transmogrify", "--input", str(inp), "--output", "x").returncode == 2
+
+
+def test_apply_edge_order_follows_the_reference(tmp_path):
+    """quake_cli.cpp:259-296: format, kernel and bias are parsed, then the input
+    is read, then the op dispatched; --coeffs is parsed only by softmax and
+    exp/QuAKE2. So an unknown op reports the missing input first (exit 3)."""
+    inp = tmp_path / "in.csv"
+    inp.write_text("0.5\n-1\n")
+    missing = str(tmp_path / "missing.csv")
+    assert run("--op", "transmogrify", "--input", missing, "--output", "x").returncode == 3
+    assert run("--op", "transmogrify", "--input", str(inp), "--output", "x").returncode == 2
+    assert run("--op", "gelu", "--coeffs", "bogus", "--input", missing, "--output", "x").returncode == 3
+    assert run("--op", "softmax", "--coeffs", "bogus", "--input", missing,
+               "--output", "x").returncode == 3
+    assert run("--op", "softmax", "--coeffs", "bogus", "--input", str(inp),
+               "--output", "x").returncode == 2
+
+
+@pytest.mark.gpu
+def test_apply_ignores_coeffs_where_the_reference_does(tmp_path):
+    inp, out = tmp_path / "in.csv", tmp_path / "out.csv"
+    inp.write_text("0.5\n-1\n")
+    for op, kern in (("gelu", "quake2"), ("logistic", "quake2"), ("exp", "quake"), ("exp", "exact")):
+        r = run("--op", op, "--kernel", kern, "--coeffs", "bogus", "--input", str(inp),
+                "--output", str(out))
+        assert r.returncode == 0, (op, kern, r.stderr)
+    r = run("--op", "exp", "--kernel", "quake2", "--coeffs", "bogus", "--input", str(inp),
+            "--output", str(out))
+    assert r.returncode == 2
 
 
 @pytest.mark.gpu

@@ -135,14 +135,13 @@ void set_devices(const std::string& list) {
 }
 
 int run_apply(const Args& a) {
-  // reference order: format, kernel, bias, then the input (quake_cli.cpp:259-264)
+  // reference order (quake_cli.cpp:259-296): format, kernel, bias, then the
+  // input is read; the op is dispatched only afterwards (an unknown op with a
+  // missing input is an I/O error, exit 3), and --coeffs is parsed only where
+  // it is used (softmax, exp with QuAKE2), so other ops ignore a bad value
   const auto format = parse_format(a.format);
   const auto kernel = parse_kernel(a.kernel);
   const auto bias = parse_bias(a.bias);
-  const auto quad = parse_quad(a.coeffs);
-  if (a.op != "softmax" && a.op != "gelu" && a.op != "logistic" && a.op != "exp") {
-    throw UsageError("unknown op: " + a.op);
-  }
   set_devices(a.devices);
   const std::vector<float> in = quake::io::read_buffer(a.input, format);
   std::vector<float> out(in.size());
@@ -150,26 +149,30 @@ int run_apply(const Args& a) {
     quake::SoftmaxParams params;
     params.temperature = a.temperature;
     params.centering_bias = bias;
-    params.quad = quad;
+    params.quad = parse_quad(a.coeffs);
     quake::softmax_rows(in, a.cols == 0 ? in.size() : a.cols, params, kernel, out);
   } else if (a.op == "gelu") {
     quake::gelu_buffer(in, out, kernel, bias);
   } else if (a.op == "logistic") {
     quake::logistic_buffer(in, out, kernel, bias);
-  } else if (kernel == quake::KernelChoice::Exact) {  // exp
-    if (qk_status s = qk_exp_buffer(in.data(), in.size(), out.data(), out.size(), QK_EXACT)) {
-      if (qk_is_invalid_argument(s)) throw std::invalid_argument(qk_last_error());
-      throw std::runtime_error(qk_last_error());
+  } else if (a.op == "exp") {
+    if (kernel == quake::KernelChoice::Exact) {
+      if (qk_status s = qk_exp_buffer(in.data(), in.size(), out.data(), out.size(), QK_EXACT)) {
+        if (qk_is_invalid_argument(s)) throw std::invalid_argument(qk_last_error());
+        throw std::runtime_error(qk_last_error());
+      }
+    } else {
+      const quake::AffineCoeffs c =
+          quake::natural_exp_coeffs(quake::resolve_centering_bias(kernel, bias));
+      const quake::ClampRange r = quake::clamp_for(c);
+      if (kernel == quake::KernelChoice::Quake) {
+        quake::quake_buffer(in, out, c, r);
+      } else {
+        quake::quake2_buffer(in, out, c, parse_quad(a.coeffs), r);
+      }
     }
   } else {
-    const quake::AffineCoeffs c =
-        quake::natural_exp_coeffs(quake::resolve_centering_bias(kernel, bias));
-    const quake::ClampRange r = quake::clamp_for(c);
-    if (kernel == quake::KernelChoice::Quake) {
-      quake::quake_buffer(in, out, c, r);
-    } else {
-      quake::quake2_buffer(in, out, c, quad, r);
-    }
+    throw UsageError("unknown op: " + a.op);
   }
   quake::io::write_buffer(a.output, out, format);
   return kExitOk;
