@@ -367,7 +367,9 @@ int or_softmax_rows_ordered(const float* mat, size_t n, size_t cols, float tempe
     const int st = row_max_checked(mat + r * cols, cols, &m);
     if (st != OR_OK) return st;
   }
-  const long long nchunks = (long long)(cols / (size_t)width);
+  /* chunks of `width` consecutive elements; with cols % width != 0 the last
+     chunk is partial and adds only its valid elements (kSpan, width 4) */
+  const long long nchunks = (long long)((cols + (size_t)width - 1) / (size_t)width);
   if (slice <= 0) { slice = nchunks; cluster = 1; balanced = 0; }
   float part[1024];
   for (size_t r = 0; r < rows; ++r) {
@@ -393,7 +395,10 @@ int or_softmax_rows_ordered(const float* mat, size_t n, size_t cols, float tempe
       for (int l = 0; l < lanes; ++l) {
         float s = 0.0f;
         for (long long j = l; j < cnt; j += lanes) {
-          for (int e = 0; e < width; ++e) s = s + y[(b + j) * width + e];
+          for (int e = 0; e < width; ++e) {
+            const size_t idx = (size_t)((b + j) * width + e);
+            if (idx < cols) s = s + y[idx];
+          }
         }
         part[l] = s;
       }

@@ -74,6 +74,7 @@ enum class SmVariant : int {
   kRowsSmem = 10,   // one thread per row, rows staged through smem (coalesced), <= 64 cols
   kSubWarp = 11,    // G lanes per aligned row, up to 8 float4 chunks each (lanes = G)
   kTiles = 12,      // unaligned rows in TMA row tiles through smem, G lanes per row
+  kSpan = 13,       // row spans through smem at any address / length, float4 chunks, G lanes
 };
 
 struct SmPlan {

@@ -13,7 +13,7 @@ import paper_2412_00408_b200 as qk  # noqa: E402
 from paper_2412_00408_b200 import _lib  # noqa: E402
 
 NAMES = {1: "warp_scalar", 2: "smem", 3: "global3", 4: "pipe", 6: "pipe_l2", 7: "pipe_s",
-         9: "thread_row", 10: "rows_smem", 11: "subwarp", 12: "tiles"}
+         9: "thread_row", 10: "rows_smem", 11: "subwarp", 12: "tiles", 13: "span"}
 # IOFF / OOFF: input / output offsets in floats (0-3) from a 16-byte boundary
 IOFF, OOFF = int(os.environ.get("IOFF", "0")), int(os.environ.get("OOFF", "0"))
 L = _lib.lib()

@@ -150,7 +150,7 @@ def test_results_do_not_depend_on_the_address(cols):
     out_all = torch.empty(n + 4, device="cuda")
     for kern in (QUAKE, QUAKE2):
         plan = qk.softmax_plan(cols, True, K(kern))
-        assert plan["width"] == (4 if cols % 4 == 0 else 1), plan
+        assert plan["width"] == (4 if cols % 4 == 0 or plan["variant"] == 13 else 1), plan
         ref = None
         for io, oo in ((0, 0), (1, 1), (2, 3), (3, 0), (0, 2), (1, 0)):
             xd = xd_all[io: io + n]
@@ -458,3 +458,38 @@ def test_in_place_matches_out_of_place(cols):
     qk.softmax_rows(xi, cols, p, K.Quake2, out=xi)
     torch.cuda.synchronize()
     assert torch.equal(y.view(torch.int32), xi.view(torch.int32)), cols
+
+
+@pytest.mark.parametrize("cols", [17, 21, 31, 33, 63, 66, 97, 130, 161, 197, 257, 513, 1001, 1535])
+@pytest.mark.parametrize("rows", [1, 37, 300])
+def test_row_spans_keep_the_declared_order(cols, rows, plan_opts):
+    """kSpan (row spans through smem, row-relative float4 chunks with a partial
+    last chunk; default for unaligned 17-192 columns, QK_SM_SPAN=2 up to 1536):
+    bit-exact against the ordered restatement with partial last spans, x86 and
+    clamped rows interleaved, and at input/output offsets of 0-3 floats."""
+    plan_opts(QK_SM_SPAN=2)
+    R = restatement()
+    rng = np.random.default_rng(cols * 13 + rows)
+    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
+    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
+    x = x.ravel()
+    n = x.size
+    for kern in (QUAKE, QUAKE2):
+        plan = qk.softmax_plan(cols, True, K(kern))
+        if cols % 4:
+            assert plan["variant"] == 13 and plan["width"] == 4, plan
+        want = R.softmax_rows_ordered(x, cols, plan, 0.5, kern)
+        for io, oo in ((0, 0), (1, 3), (2, 2), (3, 1)):
+            xb = torch.zeros(n + 4, device="cuda")
+            xb[io:io + n] = torch.from_numpy(x).cuda()
+            ob = torch.full((n + 4,), 5.0, device="cuda")
+            qk.softmax_rows(xb[io:io + n], cols, qk.SoftmaxParams(temperature=0.5), K(kern),
+                            out=ob[oo:oo + n])
+            assert_bitexact(ob[oo:oo + n].cpu().numpy(), want,
+                            f"span cols={cols} rows={rows} k={kern} in+{io} out+{oo}")
+            assert ob[:oo].eq(5.0).all() and ob[oo + n:].eq(5.0).all()
+    xb = x.copy()
+    xb[-1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
