@@ -150,8 +150,8 @@ def test_softmax_plan_geometry():
         p = qk.softmax_plan(cols, False)
         assert (p["variant"], p["width"]) == (13, 4), (cols, p)
         assert p["lanes"] * p["vpt"] * 4 >= cols and p["lanes"] & (p["lanes"] - 1) == 0
-    p = qk.softmax_plan(13, False)  # unaligned 11-16: one thread per row
-    assert (p["variant"], p["lanes"]) == (9, 1)
+    p = qk.softmax_plan(13, False)  # unaligned 11-16: one thread per row via smem
+    assert (p["variant"], p["lanes"], p["width"]) == (10, 1, 1)
     p = qk.softmax_plan(1100)  # aligned 1025-1536: a full warp per row
     assert (p["variant"], p["lanes"], p["vpt"]) == (11, 32, 12)
     p = qk.softmax_plan(513, False)
