@@ -152,6 +152,17 @@ void qk_release_workspace(void);
  * of free HBM). Shards whose host-side spans exceed it stream through rings
  * of 64 MiB chunk buffers, softmax with a validation pass first. */
 void qk_set_workspace_limit(size_t bytes);
+/* Overlapped write-back of qk_softmax_rows with pinned host spans on both
+ * sides: `threads` host threads test the shard for non-finite values from its
+ * last element backwards while the device validates the uploaded chunks from
+ * the front; once the two fronts meet, every row is validated (the
+ * reference's validate-before-write order, nonlin.cpp:176-180) and the
+ * download runs under the rest of the upload. The host threads test exponent
+ * bits only; every output value comes from the kernels. threads < 0:
+ * automatic (host CPUs, at most 16; QK_HOST_SCAN in the environment
+ * overrides), 0: off (the device validates alone). Used for shards of at
+ * least `min_bytes` (default 64 MiB). */
+void qk_set_host_validation(int32_t threads, size_t min_bytes);
 /* Softmax planner knobs (the QK_SM_* measurement options, read from the
  * environment once at first use): set `name` to `value`, or unset it when
  * `clear` != 0; name = NULL clears every option. Plans are cached per

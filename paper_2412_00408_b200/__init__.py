@@ -12,7 +12,7 @@ from .quake import (AffineCoeffs, ClampRange, FpFormat, GeluConstants, KernelCho
                     get_devices, kernel_name, logistic, logistic_buffer, natural_exp_coeffs,
                     negated_natural_exp_coeffs, quake, quake2, quake2_buffer, quake_buffer,
                     plan_override, release_workspace, resolve_centering_bias, set_device_shards,
-                    set_devices, set_plan_override, set_workspace_limit, softmax_plan,
+                    set_devices, set_host_validation, set_plan_override, set_workspace_limit, softmax_plan,
                     softmax_row, softmax_rows)
 from ._lib import LIB_PATH, lib
 

@@ -119,6 +119,7 @@ SIGNATURES = {
     "qk_set_devices": (c_int, [POINTER(c_int), c_int]),
     "qk_set_device_shards": (c_int, [POINTER(c_int), c_int]),
     "qk_set_workspace_limit": (None, [c_size_t]),
+    "qk_set_host_validation": (None, [c_int32, c_size_t]),
     "qk_set_plan_override": (c_int, [c_char_p, c_int32, c_int32]),
     "qk_get_devices": (c_int, [POINTER(c_int), c_int]),
     "qk_release_workspace": (None, []),

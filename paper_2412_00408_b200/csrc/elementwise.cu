@@ -314,7 +314,19 @@ __global__ void __launch_bounds__(kThreads) check_finite_kernel(const float* __r
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, 1u);
 }
 
+// One store to mapped pinned host memory (a plain launch: it starts after the
+// preceding kernels of the stream have completed and their atomics landed).
+__global__ void publish_flag_kernel(const uint32_t* __restrict__ flags, uint32_t* slot) {
+  *reinterpret_cast<volatile uint32_t*>(slot) = *flags | kFlagPublished;
+  __threadfence_system();
+}
+
 }  // namespace
+
+cudaError_t launch_publish_flag(const uint32_t* flags, uint32_t* slot, cudaStream_t stream) {
+  publish_flag_kernel<<<1, 1, 0, stream>>>(flags, slot);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_check_finite(const float* x, size_t n, uint32_t* flags, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;

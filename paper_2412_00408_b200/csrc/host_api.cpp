@@ -13,9 +13,11 @@
 //    replacement of parallel_chunks (parallel.hpp:43-68).
 // Reference paths cited relative to /root/reference/proj/.
 #include <cuda_runtime.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <barrier>
 #include <cmath>
 #include <cstdlib>
@@ -170,6 +172,12 @@ struct Workspace {
   size_t out_cap = 0;
   uint32_t* d_flags = nullptr;
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  // overlapped write-back (run_softmax_host): download stream, one event and
+  // one mapped pinned flag slot per chunk
+  cudaStream_t dl = nullptr;
+  uint32_t* h_slots = nullptr;
+  size_t slot_cap = 0;
+  std::vector<cudaEvent_t> events;
 };
 
 std::mutex g_ws_mu;
@@ -217,6 +225,27 @@ qk_status ensure_streams(Workspace& w) {
   if (w.streams[0] == nullptr) {
     for (auto& s : w.streams) QK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
     QK_CUDA(cudaMalloc(&w.d_flags, sizeof(uint32_t)), "cudaMalloc(flags)");
+  }
+  return QK_OK;
+}
+
+// Download stream, `n` chunk events and `n` mapped pinned flag slots.
+qk_status ensure_chunk_state(Workspace& w, size_t n) {
+  if (w.dl == nullptr) QK_CUDA(cudaStreamCreateWithFlags(&w.dl, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (n > w.slot_cap) {
+    if (w.h_slots) cudaFreeHost(w.h_slots);
+    w.h_slots = nullptr;
+    w.slot_cap = 0;
+    const size_t want = std::max<size_t>(n, 64);
+    QK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w.h_slots), want * sizeof(uint32_t),
+                          cudaHostAllocPortable | cudaHostAllocMapped),
+            "cudaHostAlloc(flag slots)");
+    w.slot_cap = want;
+  }
+  while (w.events.size() < n) {
+    cudaEvent_t e = nullptr;
+    QK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    w.events.push_back(e);
   }
   return QK_OK;
 }
@@ -557,6 +586,103 @@ qk_status validate_sm(const char* who, size_t n, size_t cols, const qk_softmax_p
   return QK_OK;
 }
 
+// ---- overlapped write-back: the host validates the tail of the shard ----
+// The contract (every row validated before the first byte reaches `out`,
+// nonlin.cpp:176-180) keeps the download behind the validation of the LAST
+// row. With the device validating alone that is the end of the upload, and
+// the two PCIe directions never overlap. Here host threads test the shard for
+// non-finite values from its last element backwards while the device
+// validates it from the front (the max pass of each uploaded chunk's softmax
+// kernel); when the two fronts meet every row is validated, and the download
+// of the computed chunks runs under the upload of the rest. The host threads
+// only test exponent bits — every output value still comes from the kernels.
+std::atomic<int> g_scan_threads{-1};                       // < 0: automatic; 0: off
+std::atomic<size_t> g_scan_min_bytes{size_t{64} << 20};    // per shard
+
+int scan_threads_auto() {
+  static const int n = [] {
+    const char* v = std::getenv("QK_HOST_SCAN");
+    if (v != nullptr && *v != '\0') return std::max(0, std::atoi(v));
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    int c = sched_getaffinity(0, sizeof(set), &set) == 0 ? CPU_COUNT(&set) : 0;
+    if (c <= 0) c = static_cast<int>(std::thread::hardware_concurrency());
+    return std::clamp(c, 1, 16);
+  }();
+  return n;
+}
+
+bool has_non_finite(const uint32_t* w, size_t n) {
+  // exponent all ones <=> (w & 0x7fffffff) >= 0x7f800000 <=> the sum carries into bit 31
+  uint32_t acc = 0;
+  for (size_t i = 0; i < n; ++i) acc |= (w[i] & 0x7fffffffu) + 0x00800000u;
+  return (acc >> 31) != 0;
+}
+
+class TailScan {
+ public:
+  static constexpr size_t kBlock = size_t{256} << 10;  // elements per claim (1 MiB)
+
+  TailScan(const float* x, size_t n, int threads)
+      : w_(reinterpret_cast<const uint32_t*>(x)), n_(n), nblocks_((n + kBlock - 1) / kBlock),
+        done_(new std::atomic<uint8_t>[nblocks_]) {
+    for (size_t k = 0; k < nblocks_; ++k) done_[k].store(0, std::memory_order_relaxed);
+    for (int t = 0; t < threads; ++t) pool_.emplace_back([this] { work(); });
+  }
+  ~TailScan() { finish(); }
+  TailScan(const TailScan&) = delete;
+  TailScan& operator=(const TailScan&) = delete;
+
+  // Leading elements the device has validated so far (blocks below stop the scan).
+  void device_front(size_t elems) { front_.store(elems, std::memory_order_release); }
+  bool bad() const { return bad_.load(std::memory_order_acquire); }
+  // First element of the suffix the host has finished scanning.
+  size_t host_front() {
+    while (contig_ < nblocks_ && done_[contig_].load(std::memory_order_acquire)) ++contig_;
+    return contig_ * kBlock >= n_ ? 0 : n_ - contig_ * kBlock;
+  }
+  void finish() {
+    stop_.store(true, std::memory_order_release);
+    for (auto& t : pool_) t.join();
+    pool_.clear();
+  }
+
+ private:
+  void work() {
+    while (!stop_.load(std::memory_order_acquire)) {
+      const size_t k = next_.fetch_add(1, std::memory_order_relaxed);  // k-th block from the back
+      if (k >= nblocks_) return;
+      const size_t end = n_ - k * kBlock;
+      const size_t begin = end > kBlock ? end - kBlock : 0;
+      // blocks are claimed in descending order and the device front only
+      // grows: once one is covered, every later claim is too
+      if (end <= front_.load(std::memory_order_acquire)) return;
+      if (has_non_finite(w_ + begin, end - begin)) {
+        bad_.store(true, std::memory_order_release);
+        return;
+      }
+      done_[k].store(1, std::memory_order_release);
+    }
+  }
+
+  const uint32_t* w_;
+  size_t n_, nblocks_;
+  std::unique_ptr<std::atomic<uint8_t>[]> done_;
+  std::atomic<size_t> next_{0}, front_{0};
+  std::atomic<bool> stop_{false}, bad_{false};
+  std::vector<std::thread> pool_;
+  size_t contig_ = 0;  // polling thread only
+};
+
+bool pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 // softmax_rows over host or device spans (nonlin.cpp:162-189). The contract:
 // every row is validated before anything reaches `out` (nonlin.cpp:176-180),
 // across all shards. Per shard, one of two schedules:
@@ -630,6 +756,21 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
     };
     // Phase 1: upload + (softmax into the workspace | validation pass).
     const bool compute_now = resident && !out_dev;
+    const size_t nchunks = (nrows + chunk_rows - 1) / chunk_rows;
+    // overlapped write-back (see TailScan): pinned host spans on both sides
+    // (pageable copies are staged synchronously: nothing to overlap)
+    int scan_threads = g_scan_threads.load();
+    if (scan_threads < 0) scan_threads = scan_threads_auto();
+    scan_threads = scan_threads > 0 ? std::max<int>(1, scan_threads / static_cast<int>(devs.size())) : 0;
+    const bool overlap = ss == QK_OK && compute_now && scan_threads > 0 && nchunks >= 2 &&
+                         shard_elems * sizeof(float) >= g_scan_min_bytes.load() && pinned_host(m) &&
+                         pinned_host(out);
+    if (overlap) ss = ensure_chunk_state(w, nchunks);
+    std::unique_ptr<TailScan> scan;
+    if (overlap && ss == QK_OK) {
+      std::memset(w.h_slots, 0, nchunks * sizeof(uint32_t));
+      scan = std::make_unique<TailScan>(m + rb * cols, shard_elems, scan_threads);
+    }
     size_t ci = 0;
     for (size_t r0 = 0; ss == QK_OK && r0 < nrows; r0 += chunk_rows, ++ci) {
       const size_t cr = std::min(chunk_rows, nrows - r0);
@@ -641,14 +782,56 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
                                                        sp, w.d_flags, str)
                                   : qk::launch_check_finite(dsrc, cr * cols, w.d_flags, str);
       if (e != cudaSuccess) ss = cuda_fail(e, compute_now ? "softmax kernel" : "validation kernel");
+      if (scan && ss == QK_OK) {
+        // the chunk's verdict goes to its host slot; its event gates its download
+        e = qk::launch_publish_flag(w.d_flags, w.h_slots + ci, str);
+        if (e == cudaSuccess) e = cudaEventRecord(w.events[ci], str);
+        if (e != cudaSuccess) ss = cuda_fail(e, "publish flag");
+      }
     }
     uint32_t flags = 0;
-    for (auto& str : w.streams) {
-      if (str && cudaStreamSynchronize(str) != cudaSuccess && ss == QK_OK) ss = fail(QK_ERR_CUDA, "stream sync");
-    }
-    if (ss == QK_OK && cudaMemcpy(&flags, w.d_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
-                           cudaSuccess) {
-      ss = fail(QK_ERR_CUDA, "D2H(flags)");
+    if (scan && ss == QK_OK) {
+      // wait until the device front (chunks validated, in order) reaches the
+      // host front (suffix scanned), or either side finds a non-finite value
+      volatile const uint32_t* slots = w.h_slots;
+      size_t gchunks = 0;
+      for (;;) {
+        while (gchunks < nchunks && (slots[gchunks] & qk::kFlagPublished)) {
+          flags |= slots[gchunks] & 1u;
+          ++gchunks;
+        }
+        const size_t front = std::min(gchunks * chunk_rows, nrows) * cols;
+        scan->device_front(front);
+        if ((flags & 1u) || scan->bad() || front >= scan->host_front()) break;
+        if (gchunks < nchunks) {
+          const cudaError_t q = cudaEventQuery(w.events[gchunks]);
+          if (q == cudaSuccess && !(slots[gchunks] & qk::kFlagPublished)) {
+            // the chunk's stream has passed its event but the slot never arrived
+            ss = fail(QK_ERR_CUDA, "softmax: flag slot not published");
+            break;
+          }
+          if (q != cudaSuccess && q != cudaErrorNotReady) {
+            ss = cuda_fail(q, "softmax chunk");
+            break;
+          }
+          cudaGetLastError();  // cudaErrorNotReady from the query
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+      scan->finish();
+      if (scan->bad()) flags |= 1u;
+      if (flags & 1u) {
+        // out stays untouched; let the queued uploads and kernels drain
+        for (auto& str : w.streams) cudaStreamSynchronize(str);
+      }
+    } else {
+      for (auto& str : w.streams) {
+        if (str && cudaStreamSynchronize(str) != cudaSuccess && ss == QK_OK) ss = fail(QK_ERR_CUDA, "stream sync");
+      }
+      if (ss == QK_OK && cudaMemcpy(&flags, w.d_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
+                             cudaSuccess) {
+        ss = fail(QK_ERR_CUDA, "D2H(flags)");
+      }
     }
     if (flags & 1u) non_finite.store(true);
     if (ss != QK_OK) abort_all.store(true);  // no shard writes back
@@ -664,6 +847,12 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
       cudaStream_t str = w.streams[ci % kRing];
       float* hdst = out + (rb + r0) * cols;
       if (compute_now) {
+        if (scan) {
+          // on the download stream, behind the chunk's own kernel only: the
+          // upload streams still carry the rest of the shard
+          str = w.dl;
+          QK_CUDA(cudaStreamWaitEvent(str, w.events[ci], 0), "cudaStreamWaitEvent");
+        }
         QK_CUDA(cudaMemcpyAsync(hdst, w.d_out + r0 * cols, cr * cols * sizeof(float),
                                 cudaMemcpyDeviceToHost, str),
                 "D2H");
@@ -683,6 +872,7 @@ qk_status run_softmax_host(const float* m, size_t n, size_t cols, const qk_softm
       }
     }
     for (auto& str : w.streams) QK_CUDA(cudaStreamSynchronize(str), "stream sync");
+    if (scan) QK_CUDA(cudaStreamSynchronize(w.dl), "stream sync");
     return QK_OK;
   });
   if (non_finite.load() && (s == QK_OK || s == QK_ERR_NON_FINITE)) {
@@ -751,6 +941,11 @@ int qk_get_devices(int* devices, int cap) {
 
 void qk_set_workspace_limit(size_t bytes) { g_ws_limit.store(bytes); }
 
+void qk_set_host_validation(int32_t threads, size_t min_bytes) {
+  g_scan_threads.store(threads);
+  g_scan_min_bytes.store(min_bytes);
+}
+
 qk_status qk_set_plan_override(const char* name, int32_t value, int32_t clear) {
   if (!qk::set_plan_opt(name, value, clear != 0)) {
     return fail(QK_ERR_BAD_ARGUMENT, std::string("set_plan_override: unknown option ") +
@@ -765,7 +960,7 @@ void qk_release_workspace(void) {
   for (auto& wp : g_ws) {
     Workspace& w = *wp;
     std::lock_guard<std::mutex> lk(w.mu);
-    if (w.streams[0] == nullptr && w.d_in == nullptr && w.d_out == nullptr) continue;
+    if (w.streams[0] == nullptr && w.d_in == nullptr && w.d_out == nullptr && w.dl == nullptr) continue;
     cudaSetDevice(w.dev);
     if (w.d_in) cudaFree(w.d_in);
     if (w.d_out) cudaFree(w.d_out);
@@ -774,6 +969,13 @@ void qk_release_workspace(void) {
       if (st) cudaStreamDestroy(st);
       st = nullptr;
     }
+    if (w.dl) cudaStreamDestroy(w.dl);
+    if (w.h_slots) cudaFreeHost(w.h_slots);
+    for (cudaEvent_t e : w.events) cudaEventDestroy(e);
+    w.events.clear();
+    w.dl = nullptr;
+    w.h_slots = nullptr;
+    w.slot_cap = 0;
     w.d_in = w.d_out = nullptr;
     w.d_flags = nullptr;
     w.in_cap = w.out_cap = 0;

@@ -50,6 +50,12 @@ cudaError_t launch_elementwise(EwOp op, const float* in, float* out, size_t n,
 // Validation pass: OR 1 into *flags (device) when x[0..n) holds a non-finite value.
 cudaError_t launch_check_finite(const float* x, size_t n, uint32_t* flags, cudaStream_t stream);
 
+// Publishes *flags (device) to *slot (mapped pinned host memory) as
+// `*flags | kFlagPublished`, stream-ordered after the kernels that raise it:
+// the host-span driver polls the slot instead of synchronising the stream.
+constexpr uint32_t kFlagPublished = 0x80000000u;
+cudaError_t launch_publish_flag(const uint32_t* flags, uint32_t* slot, cudaStream_t stream);
+
 // ---- row softmax ----
 
 enum class SmKernel : int { kExact = 0, kQuake = 1, kQuake2 = 2, kQuake2General = 3,

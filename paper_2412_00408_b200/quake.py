@@ -264,6 +264,14 @@ def set_workspace_limit(nbytes: int) -> None:
     _lib.lib().qk_set_workspace_limit(int(nbytes))
 
 
+def set_host_validation(threads: int = -1, min_bytes: int = 64 << 20) -> None:
+    """Overlapped write-back of host-span softmax_rows (pinned spans): host
+    threads validate the shard's tail while the device validates its front,
+    so the download starts before the upload ends. threads < 0 automatic,
+    0 off (the device validates alone)."""
+    _lib.lib().qk_set_host_validation(int(threads), int(min_bytes))
+
+
 def set_plan_override(name: Optional[str], value: int = 0, clear: bool = False) -> None:
     """Set (or with ``clear`` unset) a softmax planner knob (QK_SM_*); name
     None clears all. The environment is read once, at first use."""

@@ -39,6 +39,7 @@ def _reset_driver():
     yield
     qk.set_devices([])
     qk.set_workspace_limit(0)
+    qk.set_host_validation(-1, 64 << 20)
 
 
 def _same(a, b, what):
@@ -153,6 +154,46 @@ def test_streamed_host_path_matches_resident():
         _same(ye, qk.logistic_buffer(torch.from_numpy(xe).cuda(), K.Quake2), "ring logistic")
         qk.set_workspace_limit(0)
         qk.set_devices([])
+    qk.release_workspace()
+
+
+def test_overlapped_write_back_keeps_bits_and_contract():
+    """Pinned host spans on both sides: host threads validate the shard from
+    its last element backwards while the device validates the uploaded chunks
+    from the front, and the download starts when the fronts meet
+    (qk_set_host_validation). Same bits as the device path; a non-finite value
+    anywhere (device side, host side, the meeting region) is reported before
+    anything reaches `out` (nonlin.cpp:176-180)."""
+    L = _lib.lib()
+    cols, rows = 4096, 10000  # 164 MB: three 64 MiB chunks
+    n = rows * cols
+    xd = CFG5.device((0, n))
+    want = qk.softmax_rows(xd, cols, qk.SoftmaxParams(), K.Quake2)
+    hx = xd.cpu().pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    prm = qk.SoftmaxParams()._c()
+    torch.cuda.synchronize()
+
+    def call(src, dst):
+        return L.qk_softmax_rows(src.data_ptr(), n, cols, ctypes.byref(prm), int(K.Quake2),
+                                 dst.data_ptr(), n)
+
+    for threads, shards in ((4, 1), (2, 2), (0, 1), (-1, 1)):
+        qk.set_device_shards([0] * shards)
+        qk.set_host_validation(threads, 1 << 20)
+        for rep in range(3):
+            hy.fill_(-7.0)
+            assert call(hx, hy) == 0, _lib.last_error()
+            assert torch.equal(hy.cuda(), want), (threads, shards, rep)
+        for pos in (5, n // 3, n // 2 + 17, n - 3 * cols, n - 1):
+            hb = hx.clone().pin_memory()
+            hb[pos] = float("nan") if pos % 2 else float("-inf")
+            hy.fill_(123.0)
+            assert call(hb, hy) == 5, (threads, shards, pos, _lib.last_error())
+            assert bool(torch.all(hy == 123.0)), (threads, shards, pos)
+        # and the next clean call is unaffected
+        assert call(hx, hy) == 0
+        assert torch.equal(hy.cuda(), want)
     qk.release_workspace()
 
 
