@@ -514,14 +514,15 @@ def main():
     peak, peak_kind = hbm_peak()
     achieved = BYTES_PER_ELEM * n_local / (kern_ms * 1e-3) / 1e9
     plan = qk.softmax_plan(w.cols, True, qk.KernelChoice.Quake2)
-    kernel_name = {1: "softmax_warp_scalar", 2: "softmax_smem",
+    kernel_name = {2: "softmax_smem",
                    3: "softmax_global3", 4: "softmax_pipe (TMA pipeline, cluster)",
                    6: "softmax_pipe_l2 (long-row pipeline, cluster)",
                    7: "softmax_pipe_s (scalar-lane pipeline, cluster)",
                    9: "softmax_thread_row (one thread per row)",
                    10: "softmax_rows_smem (one thread per row, smem tile)",
                    11: "softmax_subwarp (G lanes per row)",
-                   12: "softmax_tiles (TMA row tiles)"}[plan["variant"]]
+                   13: "softmax_span (row spans through smem)",
+                   14: "softmax_wring (per-agent TMA rings)"}[plan["variant"]]
     line = {
         "metric": "elements/s", "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": region_ms / args.steps,

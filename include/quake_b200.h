@@ -109,15 +109,20 @@ typedef struct {
 /* Softmax launch plan (introspection; the reduction geometry that fixes the
  * summation order, see softmax.cu). */
 typedef struct {
-  int32_t variant; /* 1 warp/scalar, 2 smem(+cluster), 3 global 3-sweep,
+  int32_t variant; /* 2 smem(+cluster), 3 global 3-sweep,
                       4 persistent TMA pipeline (+cluster),
                       6 long-row pipeline (one stage, prefix refilled early),
                       7 scalar-lane pipeline (cols % 4 != 0),
                       9 one thread per row (<= 16 cols; lanes = 1: sequential sum),
                       10 one thread per row through an smem tile (lanes = 1),
                       11 G lanes per row (lanes = G, vpt = chunks per lane),
-                      12 TMA row tiles, G lanes per row (unaligned 33-200 cols);
-                      0, 5, 8: retired variants (numbers reserved) */
+                      13 row spans through smem, row-relative float4 chunks, G lanes
+                         (unaligned 17-192 cols, misaligned bases),
+                      14 per-agent TMA rings of row spans, scalar lanes (unaligned
+                         193-9216 cols; lanes = G lanes per row with vpt elements each,
+                         or vpt = 0: three sweeps by an agent of lanes/32 warps;
+                         stages = buffers per ring);
+                      0, 1, 5, 8, 12: retired variants (numbers reserved) */
   int32_t width;   /* elements per chunk: 4 when cols % 4 == 0, else 1 (any address) */
   int32_t lanes;   /* partial-sum lanes per CTA */
   int32_t cluster; /* CTAs per row */

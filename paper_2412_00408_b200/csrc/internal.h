@@ -67,10 +67,10 @@ enum class SmKernel : int { kExact = 0, kQuake = 1, kQuake2 = 2, kQuake2General 
 // Reduction geometry of one launch (also reported through qk_softmax_plan so
 // the tests can restate the exact summation order).
 enum class SmVariant : int {
-  // 0 (warp per row, float4 lanes), 5 (two-row lookahead pipeline) and 8
-  // (several short rows per warp): retired, measured slower than the kernels
-  // below; the numbers stay reserved
-  kWarpScalar = 1,  // warp per row, row in registers, scalar lanes
+  // 0 (warp per row, float4 lanes), 1 (warp per row, scalar lanes), 5
+  // (two-row lookahead pipeline), 8 (several short rows per warp) and 12
+  // (TMA row tiles): retired, measured slower than the kernels below; the
+  // numbers stay reserved
   kSmem = 2,        // CTA (or cluster of CTAs) per row, row staged in smem
   kGlobal3 = 3,     // CTA per row, three sweeps over global memory (huge rows)
   kPipe = 4,        // persistent cluster per row group, multi-stage TMA pipeline
@@ -79,8 +79,8 @@ enum class SmVariant : int {
   kThreadRow = 9,   // one thread per row (<= 16 cols): the reference's sequential order
   kRowsSmem = 10,   // one thread per row, rows staged through smem (coalesced), <= 64 cols
   kSubWarp = 11,    // G lanes per aligned row, up to 8 float4 chunks each (lanes = G)
-  kTiles = 12,      // unaligned rows in TMA row tiles through smem, G lanes per row
   kSpan = 13,       // row spans through smem at any address / length, float4 chunks, G lanes
+  kWarpRing = 14,   // per-agent (1-8 warps) TMA ring of row spans, scalar lanes: rows of cols % 4 != 0
 };
 
 struct SmPlan {
@@ -95,7 +95,7 @@ struct SmPlan {
   int stages;       // kPipe: row slices in flight per CTA
   int balanced;     // kPipe: rank r owns q (+1 if r < nchunks % cluster) chunks
   int resident;     // kPipe: clusters resident at once (occupancy API; 0 = unknown)
-  int rr;           // kWarpScalar: rows per warp (1 or 2)
+  int rr;           // kWarpRing: rows per job
   int pf;           // kPipeL2: rows bulk-prefetched into L2 ahead (0 = off)
 };
 

@@ -280,7 +280,7 @@ def set_plan_override(name: Optional[str], value: int = 0, clear: bool = False) 
 
 
 class plan_override:
-    """Context manager: ``with plan_override(QK_SM_TILES=1): ...``."""
+    """Context manager: ``with plan_override(QK_SM_RING=0): ...``."""
 
     def __init__(self, **opts):
         self.opts = opts

@@ -13,7 +13,7 @@ import paper_2412_00408_b200 as qk  # noqa: E402
 from paper_2412_00408_b200 import _lib  # noqa: E402
 
 NAMES = {1: "warp_scalar", 2: "smem", 3: "global3", 4: "pipe", 6: "pipe_l2", 7: "pipe_s",
-         9: "thread_row", 10: "rows_smem", 11: "subwarp", 12: "tiles", 13: "span"}
+         9: "thread_row", 10: "rows_smem", 11: "subwarp", 12: "tiles", 13: "span", 14: "ring"}
 # IOFF / OOFF: input / output offsets in floats (0-3) from a 16-byte boundary
 IOFF, OOFF = int(os.environ.get("IOFF", "0")), int(os.environ.get("OOFF", "0"))
 L = _lib.lib()
@@ -52,5 +52,6 @@ for cols in cols_list:
     gbs = 8 * n / us / 1e3
     print(json.dumps({"cols": cols, "aligned": cols % 4 == 0, "ioff": IOFF, "ooff": OOFF,
                       "kernel": NAMES[plan["variant"]],
-                      "lanes": plan["lanes"], "cluster": plan["cluster"], "us": round(us, 1),
+                      "lanes": plan["lanes"], "cluster": plan["cluster"], "threads": plan["threads"],
+                      "stages": plan["stages"], "smem": plan["smem"], "us": round(us, 1),
                       "gbps": round(gbs, 1), "frac": round(gbs / peak, 3)}), flush=True)

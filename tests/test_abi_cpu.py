@@ -154,8 +154,20 @@ def test_softmax_plan_geometry():
     assert (p["variant"], p["lanes"], p["width"]) == (10, 1, 1)
     p = qk.softmax_plan(1100)  # aligned 1025-1536: a full warp per row
     assert (p["variant"], p["lanes"], p["vpt"]) == (11, 32, 12)
-    p = qk.softmax_plan(513, False)
-    assert (p["variant"], p["width"]) == (1, 1)
+    # unaligned 193-9216: per-agent TMA rings, width-1 order; the register form
+    # (G lanes per row, vpt elements per lane, a multiple of four, the first
+    # vpt-4 full for every lane) up to 1024 columns, above it three sweeps by
+    # an agent of lanes/32 warps
+    for cols, lanes in ((193, 8), (229, 8), (257, 16), (513, 32), (1001, 32), (1025, 32),
+                        (2049, 64), (4097, 128), (8191, 256)):
+        p = qk.softmax_plan(cols, False)
+        assert (p["variant"], p["width"], p["lanes"]) == (14, 1, lanes), (cols, p)
+        assert p["stages"] in (3, 4) and p["cluster"] == 1
+        if cols <= 1024:
+            assert p["vpt"] % 4 == 0 and lanes * (p["vpt"] - 4) < cols <= lanes * p["vpt"], (cols, p)
+        else:
+            assert p["vpt"] == 0 and p["threads"] % lanes == 0
+        assert p["threads"] % 32 == 0 and p["smem"] <= 225 * 1024
     p = qk.softmax_plan(1 << 23)
     assert p["variant"] == 3
     for cols in (2048, 4096, 16384, 50000, 65536, 128256, 300000):

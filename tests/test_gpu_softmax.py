@@ -419,31 +419,6 @@ def test_subwarp_rows_keep_the_declared_order(cols, plan_opts):
                             f"subwarp cols={cols} k={kern} t={t} plan={plan}")
 
 
-@pytest.mark.parametrize("cols", [97, 127, 129, 161, 197, 257, 513, 577, 1001, 1023])
-@pytest.mark.parametrize("rows", [1, 37, 389])
-def test_row_tiles_keep_the_declared_order(cols, rows, plan_opts):
-    """kTiles (TMA row tiles through smem for unaligned rows, G lanes per row;
-    default for 97-200 columns, forced up to 1024 with QK_SM_TILES=1): bit-exact against the ordered restatement with full tiles, a
-    partial last tile and a single row; x86 and clamped rows interleaved."""
-    plan_opts(QK_SM_TILES=1)
-    R = restatement()
-    rng = np.random.default_rng(cols * 7 + rows)
-    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
-    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
-    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
-    x = x.ravel()
-    for kern in (QUAKE, QUAKE2):
-        plan = qk.softmax_plan(cols, False, K(kern))
-        assert plan["variant"] == 12 and plan["width"] == 1, plan
-        y = _gpu_softmax(x, cols, 1.0, kern)
-        assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, kern),
-                        f"tiles cols={cols} rows={rows} k={kern} plan={plan}")
-    xb = x.copy()
-    xb[-1] = np.nan
-    with pytest.raises(ValueError, match="non-finite"):
-        qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
-
-
 @pytest.mark.parametrize("cols", [7, 16, 31, 77, 127, 128, 257, 512, 1001, 4097, 16384, 50257,
                                   128256, 262144])
 def test_in_place_matches_out_of_place(cols):
@@ -489,6 +464,54 @@ def test_row_spans_keep_the_declared_order(cols, rows, plan_opts):
             assert_bitexact(ob[oo:oo + n].cpu().numpy(), want,
                             f"span cols={cols} rows={rows} k={kern} in+{io} out+{oo}")
             assert ob[:oo].eq(5.0).all() and ob[oo + n:].eq(5.0).all()
+    xb = x.copy()
+    xb[-1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
+
+
+@pytest.mark.parametrize("cols", [129, 161, 193, 197, 256, 257, 321, 385, 512, 513, 640, 769,
+                                  1001, 1024, 1027, 2047, 2305, 4099, 8191])
+@pytest.mark.parametrize("rows", [1, 37, 300])
+def test_warp_rings_keep_the_declared_order(cols, rows, plan_opts):
+    """kWarpRing (per-agent TMA rings of row spans; the register-resident form
+    with G lanes per row up to 1024 columns, three smem sweeps per row above,
+    by agents of 1-8 warps): bit-exact against the ordered restatement (width
+    1, `lanes` lanes) with partial last jobs, x86 and clamped rows interleaved,
+    at input/output offsets of 0-3 floats (equal and different phases), with
+    3- and 4-buffer rings and every agent size."""
+    R = restatement()
+    rng = np.random.default_rng(cols * 17 + rows)
+    x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+    x[1::9] = rng.uniform(-1e30, 1e30, (len(x[1::9]), cols))
+    x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
+    x = x.ravel()
+    n = x.size
+    sets = [dict(), dict(QK_SM_RING_NB=4, QK_SM_RING_REGS=0, QK_SM_RING_AW=1)]
+    if cols > 1024:
+        sets += [dict(QK_SM_RING_AW=aw) for aw in (2, 4, 8)]
+    for opts in sets:
+        plan_opts(QK_SM_RING=1, **opts)
+        for kern in (QUAKE, QUAKE2):
+            plan = qk.softmax_plan(cols, True, K(kern))
+            assert plan["variant"] == 14 and plan["width"] == 1, plan
+            if plan["vpt"] > 0:  # register form: G lanes per row, vpt elements per lane
+                assert cols <= 1024 and "QK_SM_RING_REGS" not in opts, plan
+                assert plan["lanes"] * (plan["vpt"] - 4) < cols <= plan["lanes"] * plan["vpt"], plan
+            else:                # three sweeps by an agent of lanes/32 warps
+                assert plan["lanes"] == 32 * opts.get("QK_SM_RING_AW", plan["lanes"] // 32), plan
+            want = R.softmax_rows_ordered(x, cols, plan, 0.5, kern)
+            for io, oo in ((0, 0), (1, 3), (2, 2), (3, 1), (1, 1)):
+                xb = torch.zeros(n + 4, device="cuda")
+                xb[io:io + n] = torch.from_numpy(x).cuda()
+                ob = torch.full((n + 4,), 5.0, device="cuda")
+                qk.softmax_rows(xb[io:io + n], cols, qk.SoftmaxParams(temperature=0.5), K(kern),
+                                out=ob[oo:oo + n])
+                assert_bitexact(ob[oo:oo + n].cpu().numpy(), want,
+                                f"ring cols={cols} rows={rows} k={kern} {opts} {plan} in+{io} out+{oo}")
+                assert ob[:oo].eq(5.0).all() and ob[oo + n:].eq(5.0).all()
+        for k in opts:
+            qk.set_plan_override(k, 0, clear=True)
     xb = x.copy()
     xb[-1] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
