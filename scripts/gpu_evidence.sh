@@ -27,3 +27,11 @@ du -sh gpurun_out
 # the 2-way split on one GPU through torchrun (correctness: fingerprints add up)
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29518 bench.py --gpus 2 --steps 10 --warmup 3 --no-extras > gpurun_out/bench_torchrun2.log 2>&1; echo "torchrun2 exit $?" >> gpurun_out/bench_torchrun2.log
 python scripts/launch_summary.py gpurun_out/launches.csv gpurun_out/launches_summary.json "$CMD" > /dev/null 2>&1
+# softmax by row length with the final planner, and the warp-ring kernel under ncu
+COLS="4,7,16,31,32,47,64,77,127,128,161,197,256,257,512,513,577,1001,1024,1025,2047,2049,4096,4097,8191,16384,16387,50000,50257,128256,151936,151937,202048,256000,262144" \
+  timeout 900 python scripts/softmax_shape_sweep.py > gpurun_out/shape_sweep.jsonl 2> gpurun_out/shape_sweep.err
+for c in 513 2049 4097; do
+  COLS=$c MODES="" REPS=1 ITERS=2 TOTAL=268435456 timeout 300 ncu --set full --clock-control none --import-source on \
+    -k regex:softmax_wring -s 2 -c 1 -o /tmp/ring_$c -f python scripts/ring_ab.py > gpurun_out/ncu_ring_$c.log 2>&1
+  python scripts/ncu_summary.py /tmp/ring_$c.ncu-rep gpurun_out/ncu_ring_$c "warp-ring softmax, $c cols, QuAKE2" > /dev/null 2>&1
+done
