@@ -29,6 +29,19 @@ xd = torch.from_numpy(xb).cuda()[1:]
 yd = qk.softmax_rows(xd, 517, qk.SoftmaxParams(), K.Quake2).cpu().numpy()
 bad += int(np.count_nonzero(yd.view(np.uint32) != R.softmax_rows_ordered(
     xb[1:], 517, qk.softmax_plan(517, False, K.Quake2), 1.0, QUAKE2).view(np.uint32)))
+# warp rings: register form (G = 8, 16, 32), three sweeps with agents of 1, 2, 4 and 8 warps;
+# aligned and misaligned bases, same and different in/out phases, partial last jobs
+for cols, rows in ((197, 37), (257, 21), (513, 13), (1001, 9), (1537, 7), (2049, 11), (4099, 9), (8191, 5)):
+    for io, oo in ((0, 0), (1, 1), (2, 3)):
+        x = (rng.standard_normal(rows * cols) * 3).astype(np.float32)
+        xb = torch.zeros(rows * cols + 4, device="cuda")
+        xb[io:io + rows * cols] = torch.from_numpy(x).cuda()
+        ob = torch.empty(rows * cols + 4, device="cuda")
+        qk.softmax_rows(xb[io:io + rows * cols], cols, qk.SoftmaxParams(), K.Quake2,
+                        out=ob[oo:oo + rows * cols])
+        want = R.softmax_rows_ordered(x, cols, qk.softmax_plan(cols, False, K.Quake2), 1.0, QUAKE2)
+        bad += int(np.count_nonzero(ob[oo:oo + rows * cols].cpu().numpy().view(np.uint32) !=
+                                    want.view(np.uint32)))
 # elementwise: vector + scalar (misaligned) paths
 x = rng.uniform(-100, 100, 100003).astype(np.float32)
 for kern in (K.Quake, K.Quake2):

@@ -5,6 +5,7 @@ import ctypes
 import json
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
@@ -30,6 +31,7 @@ cols_list = [int(c) for c in os.environ.get("COLS", "4,7,16,31,32,64,77,127,128,
                                             "577,1001,1024,2047,4096,4097,16384,50000,50257,"
                                             "128256,151936,151937,202048,256000,262144").split(",")]
 for cols in cols_list:
+    time.sleep(float(os.environ.get("SLEEP", "1.0")))  # let the clocks recover between shapes
     rows = total // cols
     n = rows * cols
     plan = qk.softmax_plan(cols, cols % 4 == 0, qk.KernelChoice.Quake2)
