@@ -1,13 +1,13 @@
 #!/bin/bash
-# Probe: ncu --set full of the warp-ring kernel at a few row lengths / forms.
+# Probe: ncu --set full of the warp-ring kernel at a few row lengths, with per-instruction counts.
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 cap() {  # cols tag env...
   local cols=$1 tag=$2; shift 2
   env "$@" COLS=$cols MODES="" REPS=1 ITERS=2 TOTAL=${TOTAL:-67108864} timeout 300 ncu --set full --clock-control none --import-source on \
-    -k regex:"softmax_wring|softmax_warp_scalar|softmax_pipe_s" -s 2 -c 1 -o /tmp/ring_$tag -f python scripts/ring_ab.py > gpurun_out/ncu_ring_$tag.log 2>&1
+    -k regex:"softmax_wring" -s 2 -c 1 -o /tmp/ring_$tag -f python scripts/ring_ab.py > gpurun_out/ncu_ring_$tag.log 2>&1
   python scripts/ncu_summary.py /tmp/ring_$tag.ncu-rep gpurun_out/ncu_ring_$tag "$tag" > /dev/null 2>&1
   python scripts/ncu_inst_sass.py /tmp/ring_$tag.ncu-rep gpurun_out/ncu_ring_${tag}_inst.txt > /dev/null 2>&1
 }
-cap 1001 sweep1001 QK_SM_RING=1 QK_SM_RING_REGS=0
-cap 513 regs513 QK_SM_RING=1
+cap 2049 a2049 QK_SM_RING=1
+cap 513 r513 QK_SM_RING=1

@@ -3,11 +3,11 @@
 A serving loop captures its per-step kernels once and replays the graph; the
 C-ABI device operators must be capturable (no capture-invalidating call such
 as cudaStreamGetDevice on the capturing stream) and a replay must read the
-buffers' current contents. Every kernel family is captured — elementwise, the
-warp-per-row softmax (float4 and scalar lanes), G lanes per row, one thread
-per row (direct and smem-tiled), TMA row tiles, the two-stage pipeline (C = 1
-and clusters), the scalar-lane pipeline and the long-row pipeline — and
-replays are compared bit for bit with eager launches.
+buffers' current contents. Every kernel family is captured — elementwise, G
+lanes per row, one thread per row (direct and smem-tiled), row spans, the
+warp rings (register form, three sweeps, agents of several warps), the
+two-stage pipeline (C = 1 and clusters), the scalar-lane pipeline and the
+long-row pipeline — and replays are compared bit for bit with eager launches.
 """
 import ctypes
 
@@ -42,10 +42,13 @@ def _ops(L, sh):
         ("softmax 128256", 128256 * 40, sm(128256, prm1, K.Quake2)),
         ("softmax 262144", 262144 * 40, sm(262144, prm1, K.Quake2)),
         ("softmax 50257 (scalar lanes)", 50257 * 40, sm(50257, prm1, K.Quake2)),
-        ("softmax 1001 (scalar warp)", 1001 * 300, sm(1001, prm1, K.Quake2)),
+        ("softmax 1001 (warp ring, 32 lanes per row)", 1001 * 300, sm(1001, prm1, K.Quake2)),
         ("softmax 48 (sub-warp)", 48 * 3000, sm(48, prm8, K.Quake)),
-        ("softmax 197 (row tiles)", 197 * 3001, sm(197, prm1, K.Quake2)),
-        ("softmax 513 (scalar warp, two rows)", 513 * 301, sm(513, prm1, K.Quake2)),
+        ("softmax 197 (warp ring, 8 lanes per row)", 197 * 3001, sm(197, prm1, K.Quake2)),
+        ("softmax 513 (warp ring, partial last job)", 513 * 301, sm(513, prm1, K.Quake2)),
+        ("softmax 1537 (warp ring, three sweeps)", 1537 * 201, sm(1537, prm1, K.Quake)),
+        ("softmax 4099 (warp ring, 4-warp agents)", 4099 * 77, sm(4099, prm1, K.Quake2)),
+        ("softmax 77 (row spans)", 77 * 3001, sm(77, prm1, K.Quake2)),
         ("softmax 16 (thread per row)", 16 * 3000, sm(16, prm8, K.Quake2)),
         ("softmax 31 (smem tile)", 31 * 3000, sm(31, prm1, K.Quake2)),
     ]

@@ -343,7 +343,7 @@ def test_long_row_pipeline_extreme_and_non_finite_rows():
 @pytest.mark.parametrize("cols", [1, 2, 3, 4, 5, 7, 8, 12, 15, 16, 17, 24, 31, 32, 33, 48, 63, 64,
                                   65])
 def test_short_rows_mixed_paths(cols):
-    """Short rows (one thread per row, smem-staged rows, sub-warp lanes, row tiles):
+    """Short rows (one thread per row, smem-staged rows, sub-warp lanes, row spans):
     bit-exact against the ordered restatement, with a row count that leaves dead
     lanes in the last warp, and x86-emulated (huge-magnitude), clamped and
     ordinary rows interleaved so neighbouring rows in one warp take different paths."""
