@@ -100,10 +100,10 @@ __device__ __forceinline__ float apply(float x, const EwParams& p) {
 
 // Two elements of the QuAKE ops with the paired FMUL2/FFMA2 sequences of
 // numerics.cuh (bit-identical to apply<OP>); other ops go element-wise.
-// `ok` is cleared when a lane left the range where the paired fast division
-// equals the IEEE one; the caller then recomputes those elements with apply.
+// The guard records the range the paired fast divisions saw; apply4 tests it
+// once per float4 and the caller recomputes a refused float4 with apply.
 template <EwOp OP, bool X86>
-__device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p, bool& ok) {
+__device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p, DivGuard& g) {
   if constexpr (X86 || !(OP == EwOp::kQuake || OP == EwOp::kQuake2 ||
                          OP == EwOp::kQuake2General || OP == EwOp::kLogisticQuake ||
                          OP == EwOp::kLogisticQuake2 || OP == EwOp::kGeluQuake ||
@@ -146,7 +146,7 @@ __device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p, bo
     } else {
       quake2_body2<false>(u0, u1, p.c0, p.c1, 0.f, 0.f, 0.f, e0, e1);
     }
-    div2_ge1(a, b, __fadd_rn(1.0f, e0), __fadd_rn(1.0f, e1), ok);
+    div2_ge1(a, b, __fadd_rn(1.0f, e0), __fadd_rn(1.0f, e1), g);
   } else {
     const float u0 = saturate_fast(a, p.lo, p.hi), u1 = saturate_fast(b, p.lo, p.hi);
     float e0, e1;
@@ -158,7 +158,7 @@ __device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p, bo
       quake2_body2<false>(u0, u1, p.c0, p.c1, 0.f, 0.f, 0.f, e0, e1);
     }
     if constexpr (OP == EwOp::kLogisticQuake || OP == EwOp::kLogisticQuake2) {
-      recip2_ge1(__fadd_rn(1.0f, e0), __fadd_rn(1.0f, e1), a, b, ok);
+      recip2_ge1(__fadd_rn(1.0f, e0), __fadd_rn(1.0f, e1), a, b, g);
     } else {
       a = e0;
       b = e1;
@@ -168,8 +168,15 @@ __device__ __forceinline__ void apply2(float& a, float& b, const EwParams& p, bo
 
 template <EwOp OP, bool X86>
 __device__ __forceinline__ float4 apply4(float4 v, const EwParams& p, bool& ok) {
-  apply2<OP, X86>(v.x, v.y, p, ok);
-  apply2<OP, X86>(v.z, v.w, p, ok);
+  DivGuard g;
+  apply2<OP, X86>(v.x, v.y, p, g);
+  apply2<OP, X86>(v.z, v.w, p, g);
+  // one range test per float4 (paired fast divisions only)
+  if constexpr (!X86 && (OP == EwOp::kGeluQuake || OP == EwOp::kGeluQuake2)) {
+    ok = div_guard_ok(g);
+  } else if constexpr (!X86 && (OP == EwOp::kLogisticQuake || OP == EwOp::kLogisticQuake2)) {
+    ok = recip_guard_ok(g);
+  }
   return v;
 }
 
