@@ -479,7 +479,7 @@ def test_warp_rings_keep_the_declared_order(cols, rows, plan_opts):
     by agents of 1-8 warps): bit-exact against the ordered restatement (width
     1, `lanes` lanes) with partial last jobs, x86 and clamped rows interleaved,
     at input/output offsets of 0-3 floats (equal and different phases), with
-    3- and 4-buffer rings and every agent size."""
+    2- and 3-buffer rings and every agent size."""
     R = restatement()
     rng = np.random.default_rng(cols * 17 + rows)
     x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
@@ -487,7 +487,7 @@ def test_warp_rings_keep_the_declared_order(cols, rows, plan_opts):
     x[4::9] = rng.uniform(-300, 40, (len(x[4::9]), cols))
     x = x.ravel()
     n = x.size
-    sets = [dict(), dict(QK_SM_RING_NB=4, QK_SM_RING_REGS=0, QK_SM_RING_AW=1)]
+    sets = [dict(), dict(QK_SM_RING_NB=3, QK_SM_RING_REGS=0, QK_SM_RING_AW=1), dict(QK_SM_RING_NB=2)]
     if cols > 1024:
         sets += [dict(QK_SM_RING_AW=aw) for aw in (2, 4, 8)]
     for opts in sets:
