@@ -146,7 +146,7 @@ def test_softmax_plan_geometry():
     for cols, aligned in ((4, True), (16, True), (7, False), (10, False)):
         p = qk.softmax_plan(cols, aligned)  # one thread per row: the sequential order
         assert (p["variant"], p["lanes"]) == (9, 1), (cols, p)
-    for cols in (17, 31, 77, 161, 190):  # unaligned 17-192: row spans, float4 chunks
+    for cols in (17, 21, 31):  # unaligned 17-32: row spans, float4 chunks
         p = qk.softmax_plan(cols, False)
         assert (p["variant"], p["width"]) == (13, 4), (cols, p)
         assert p["lanes"] * p["vpt"] * 4 >= cols and p["lanes"] & (p["lanes"] - 1) == 0
@@ -154,12 +154,13 @@ def test_softmax_plan_geometry():
     assert (p["variant"], p["lanes"], p["width"]) == (10, 1, 1)
     p = qk.softmax_plan(1100)  # aligned 1025-1536: a full warp per row
     assert (p["variant"], p["lanes"], p["vpt"]) == (11, 32, 12)
-    # unaligned 193-9216: per-agent TMA rings, width-1 order; the register form
+    # unaligned 33-20480: per-agent TMA rings, width-1 order; the register form
     # (G lanes per row, vpt elements per lane, a multiple of four, the first
     # vpt-4 full for every lane) up to 1024 columns, above it three sweeps by
     # an agent of lanes/32 warps
     prev = 0
-    for cols, g in ((193, 8), (229, 8), (257, 16), (513, 32), (1001, 32), (1025, 0), (2049, 0),
+    for cols, g in ((33, 4), (77, 4), (127, 4), (129, 8), (193, 8), (229, 8), (257, 16), (513, 32),
+                    (1001, 32), (1025, 0), (2049, 0),
                     (4097, 0), (8191, 0)):
         p = qk.softmax_plan(cols, False)
         assert (p["variant"], p["width"], p["cluster"]) == (14, 1, 1), (cols, p)

@@ -470,8 +470,9 @@ def test_row_spans_keep_the_declared_order(cols, rows, plan_opts):
         qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
 
 
-@pytest.mark.parametrize("cols", [129, 161, 193, 197, 256, 257, 321, 385, 512, 513, 640, 769,
-                                  1001, 1024, 1027, 2047, 2305, 4099, 8191])
+@pytest.mark.parametrize("cols", [33, 47, 64, 65, 97, 127, 128, 129, 161, 193, 197, 256, 257, 321, 385,
+                                  512, 513, 640, 769, 1001, 1024, 1027, 2047, 2305, 4099, 8191,
+                                  16387])
 @pytest.mark.parametrize("rows", [1, 37, 300])
 def test_warp_rings_keep_the_declared_order(cols, rows, plan_opts):
     """kWarpRing (per-agent TMA rings of row spans; the register-resident form
@@ -498,6 +499,7 @@ def test_warp_rings_keep_the_declared_order(cols, rows, plan_opts):
             if plan["vpt"] > 0:  # register form: G lanes per row, vpt elements per lane
                 assert cols <= 1024 and "QK_SM_RING_REGS" not in opts, plan
                 assert plan["lanes"] * (plan["vpt"] - 4) < cols <= plan["lanes"] * plan["vpt"], plan
+                assert plan["lanes"] == (4 if cols <= 128 else 8 if cols <= 256 else 16 if cols <= 512 else 32)
             else:                # three sweeps by an agent of lanes/32 warps
                 assert plan["lanes"] == 32 * opts.get("QK_SM_RING_AW", plan["lanes"] // 32), plan
             want = R.softmax_rows_ordered(x, cols, plan, 0.5, kern)
