@@ -1,7 +1,9 @@
 #!/bin/bash
-# Probe: warp-ring kernel (direct stores) below 193 columns vs the row-span kernel.
+# Probe: after building without relocatable device code — bench line and the unaligned-row sweep.
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
-COLS="33,41,47,49,63,65,77,97,111,127,129,145,161,177,191" \
-MODES=";QK_SM_RING=1;QK_SM_RING=1,QK_SM_RING_NB=2;QK_SM_RING=1,QK_SM_RING_NB=3" REPS=3 \
-timeout 1500 python scripts/ring_ab.py > gpurun_out/ring_short.jsonl 2> gpurun_out/ring_err.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_c.log
+COLS="47,127,197,257,385,513,769,1001,1537,2049,3001,4097,8191,12001,16387,50257" MODES="" REPS=3 \
+timeout 900 python scripts/ring_ab.py > gpurun_out/ring_c.jsonl 2> gpurun_out/ring_err.log
+COLS="512,4096,16384,50000,128256,202048,262144" MODES="" REPS=3 \
+timeout 900 python scripts/ring_ab.py >> gpurun_out/ring_c.jsonl 2>> gpurun_out/ring_err.log
