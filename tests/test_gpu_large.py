@@ -47,7 +47,9 @@ def test_elementwise_beyond_2p32():
     assert_bitexact(z[-4096:].cpu().numpy(), R.gelu_buffer(xs, QUAKE), "gelu tail")
 
 
-@pytest.mark.parametrize("cols", [512, 128256])
+# 512: sub-warp rows; 128256: cluster pipeline; 513 / 4099: warp rings (register form,
+# three sweeps by two-warp agents) — 64-bit job cursors and row offsets
+@pytest.mark.parametrize("cols", [512, 128256, 513, 4099])
 def test_softmax_rows_beyond_2p32(cols):
     R = restatement()
     rows = (1 << 32) // cols + 3
