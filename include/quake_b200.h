@@ -119,7 +119,7 @@ typedef struct {
                       13 row spans through smem, row-relative float4 chunks, G lanes
                          (unaligned 17-32 cols, misaligned bases),
                       14 per-agent TMA rings of row spans, scalar lanes (unaligned
-                         33-20480 cols; lanes = G lanes per row with vpt elements each,
+                         33-28000 cols; lanes = G lanes per row with vpt elements each,
                          or vpt = 0: three sweeps by an agent of lanes/32 warps;
                          stages = buffers per ring);
                       0, 1, 5, 8, 12: retired variants (numbers reserved) */

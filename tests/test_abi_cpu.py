@@ -154,7 +154,7 @@ def test_softmax_plan_geometry():
     assert (p["variant"], p["lanes"], p["width"]) == (10, 1, 1)
     p = qk.softmax_plan(1100)  # aligned 1025-1536: a full warp per row
     assert (p["variant"], p["lanes"], p["vpt"]) == (11, 32, 12)
-    # unaligned 33-20480: per-agent TMA rings, width-1 order; the register form
+    # unaligned 33-28000: per-agent TMA rings, width-1 order; the register form
     # (G lanes per row, vpt elements per lane, a multiple of four, the first
     # vpt-4 full for every lane) up to 1024 columns, above it three sweeps by
     # an agent of lanes/32 warps

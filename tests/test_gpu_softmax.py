@@ -472,7 +472,7 @@ def test_row_spans_keep_the_declared_order(cols, rows, plan_opts):
 
 @pytest.mark.parametrize("cols", [33, 47, 64, 65, 97, 127, 128, 129, 161, 193, 197, 256, 257, 321, 385,
                                   512, 513, 640, 769, 1001, 1024, 1027, 2047, 2305, 4099, 8191,
-                                  16387])
+                                  16387, 27999])
 @pytest.mark.parametrize("rows", [1, 37, 300])
 def test_warp_rings_keep_the_declared_order(cols, rows, plan_opts):
     """kWarpRing (per-agent TMA rings of row spans; the register-resident form
