@@ -1,5 +1,6 @@
 #!/bin/bash
 # Probe: lanes per row (G) x rows per job sweep of the register-form warp ring.
+# (run at commit acca6c1: the QK_SM_RING_G knob it used was folded into the planner afterwards)
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 : > gpurun_out/ring_g.jsonl

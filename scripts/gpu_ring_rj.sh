@@ -1,5 +1,6 @@
 #!/bin/bash
 # Probe: rows per job / ring depth sweep of the warp-ring kernel.
+# (run at commit acca6c1, the in-place + bulk-store form of the rings)
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 : > gpurun_out/ring_rj.jsonl
