@@ -202,6 +202,36 @@ def test_softmax_plan_geometry():
             assert p["smem"] <= 227 * 1024
 
 
+def test_warp_ring_plans_cover_every_unaligned_length():
+    """Every row length of cols % 4 != 0 in 33..28000 gets a warp-ring plan the
+    launcher accepts: an instantiated (lanes, vpt) pair whose unpredicated slots
+    exist and which covers the row, or a three-sweep agent of 1-8 warps; rings
+    of 2-3 buffers of whole jobs that fit a CTA's shared memory."""
+    regs = {(4, v) for v in (12, 16, 20, 24, 28, 32)} | {(g, v) for g in (8, 16, 32)
+                                                         for v in (20, 24, 28, 32)}
+    K = qk.KernelChoice
+    lengths = [c for c in list(range(33, 1100)) + list(range(1100, 28001, 37)) + [27999, 28000]
+               if c % 4]
+    for cols in lengths:
+        for kern in (K.Quake, K.Quake2):
+            p = qk.softmax_plan(cols, False, kern)
+            assert (p["variant"], p["width"], p["cluster"]) == (14, 1, 1), (cols, p)
+            if p["vpt"]:
+                assert cols <= 1024 and (p["lanes"], p["vpt"]) in regs, (cols, p)
+                assert p["lanes"] * (p["vpt"] - 4) < cols <= p["lanes"] * p["vpt"], (cols, p)
+            else:
+                assert cols > 1024 and p["lanes"] in (32, 64, 128, 256), (cols, p)
+                assert p["threads"] % p["lanes"] == 0, (cols, p)
+            assert p["stages"] in (2, 3) and 32 <= p["threads"] <= 256 and p["threads"] % 32 == 0
+            # agents * buffers * (rows per job * cols + 8 floats, rounded to 32 floats)
+            agents = p["threads"] // (p["lanes"] if not p["vpt"] else 32)
+            per_buf = p["smem"] // (agents * p["stages"])
+            assert per_buf * agents * p["stages"] == p["smem"] and per_buf % 128 == 0
+            assert per_buf >= (cols + 8) * 4 and p["smem"] <= 225 * 1024, (cols, p)
+    assert qk.softmax_plan(28001, False)["variant"] != 14
+    assert qk.softmax_plan(29, False)["variant"] == 13
+
+
 def test_cuda_calls_fail_loudly_without_gpu():
     import torch
     if torch.cuda.is_available():

@@ -520,3 +520,23 @@ def test_warp_rings_keep_the_declared_order(cols, rows, plan_opts):
     xb[-1] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
         qk.softmax_rows(torch.from_numpy(xb).cuda(), cols, qk.SoftmaxParams(), K.Quake2)
+
+
+def test_every_unaligned_row_length_up_to_1100_bitexact():
+    """Every row length of cols % 4 != 0 from 17 to 1100 columns with the default
+    planner (row spans, then every register shape of the warp rings and its
+    boundaries, then the first three-sweep lengths): bit-exact against the
+    ordered restatement, a partial last job included."""
+    R = restatement()
+    rng = np.random.default_rng(11)
+    rows = 45
+    for cols in range(17, 1101):
+        if cols % 4 == 0:
+            continue
+        x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+        x[3] = rng.uniform(-300, 40, cols)
+        x = x.ravel()
+        plan = qk.softmax_plan(cols, False, K.Quake2)
+        assert plan["variant"] == (13 if cols <= 32 else 14), (cols, plan)
+        y = _gpu_softmax(x, cols, 1.0, QUAKE2)
+        assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"cols={cols} {plan}")
