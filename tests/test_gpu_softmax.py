@@ -540,3 +540,23 @@ def test_every_unaligned_row_length_up_to_1100_bitexact():
         assert plan["variant"] == (13 if cols <= 32 else 14), (cols, plan)
         y = _gpu_softmax(x, cols, 1.0, QUAKE2)
         assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"cols={cols} {plan}")
+
+
+def test_unaligned_row_lengths_up_to_28000_bitexact():
+    """Row lengths of cols % 4 != 0 sampled from 1101 to 28000 columns (every
+    agent size of the three-sweep warp rings, the 2- and 3-buffer shapes and the
+    last length before the cluster pipeline): bit-exact against the ordered
+    restatement with the default planner."""
+    R = restatement()
+    rng = np.random.default_rng(12)
+    rows = 7
+    lengths = [c for c in list(range(1101, 28001, 61)) + [27998, 27999] if c % 4]
+    seen = set()
+    for cols in lengths:
+        x = (rng.standard_normal((rows, cols)) * 3).astype(np.float32).ravel()
+        plan = qk.softmax_plan(cols, False, K.Quake2)
+        assert plan["variant"] == 14 and plan["vpt"] == 0, (cols, plan)
+        seen.add((plan["lanes"], plan["stages"]))
+        y = _gpu_softmax(x, cols, 1.0, QUAKE2)
+        assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"cols={cols} {plan}")
+    assert {l for l, _ in seen} == {32, 64, 128, 256}, seen
