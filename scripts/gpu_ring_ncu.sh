@@ -9,5 +9,5 @@ cap() {  # cols tag env...
   python scripts/ncu_summary.py /tmp/ring_$tag.ncu-rep gpurun_out/ncu_ring_$tag "$tag" > /dev/null 2>&1
   python scripts/ncu_inst_sass.py /tmp/ring_$tag.ncu-rep gpurun_out/ncu_ring_${tag}_inst.txt > /dev/null 2>&1
 }
-cap 2049 a2049 QK_SM_RING=1
-cap 513 r513 QK_SM_RING=1
+cap ${COLS1:-513} r513
+cap ${COLS2:-77} r77
