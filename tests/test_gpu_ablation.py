@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 K = qk.KernelChoice
 
 
-@pytest.mark.parametrize("cols", [33, 512, 700, 4096, 16384, 128256, 262144])
+@pytest.mark.parametrize("cols", [33, 197, 512, 700, 1537, 4096, 4099, 16384, 128256, 262144])
 @pytest.mark.parametrize("kern", [QUAKE_UNFUSED, QUAKE2_UNFUSED])
 def test_unfused_softmax_bitexact(cols, kern):
     R = restatement()

@@ -560,3 +560,25 @@ def test_unaligned_row_lengths_up_to_28000_bitexact():
         y = _gpu_softmax(x, cols, 1.0, QUAKE2)
         assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 1.0, QUAKE2), f"cols={cols} {plan}")
     assert {l for l, _ in seen} == {32, 64, 128, 256}, seen
+
+
+@pytest.mark.parametrize("cols", [77, 197, 513, 1537, 4099, 12001])
+def test_every_kernel_kind_on_the_warp_rings(cols):
+    """Every kernel kind on rows of cols % 4 != 0 (the warp rings' register and
+    three-sweep forms, every agent size): Exact / expf / __expf within their
+    tolerances of the fp64-sum restatement, the general (minimax) quad bit-exact
+    against the ordered restatement, input/output at different phases."""
+    R = restatement()
+    rows = max(5, min(64, (1 << 20) // cols))
+    x = (np.random.default_rng(cols).standard_normal(rows * cols) * 2).astype(np.float32)
+    from oracle.oracle import EXACT
+    want = R.softmax_rows(x, cols, 0.125, EXACT, sum_mode=1)
+    for kern, tol in ((K.Exact, 1e-5), (K.Expf, 1e-5), (K.FastExp, 5e-5)):
+        assert qk.softmax_plan(cols, False, kern)["variant"] == 14
+        xd = torch.zeros(x.size + 4, device="cuda")
+        xd[1:1 + x.size] = torch.from_numpy(x).cuda()
+        y = qk.softmax_rows(xd[1:1 + x.size], cols, qk.SoftmaxParams(temperature=0.125), kern)
+        assert max_rel(y.cpu().numpy(), want) <= tol, (cols, kern)
+    plan = qk.softmax_plan(cols, False, K.Quake2)
+    y = _gpu_softmax(x, cols, 0.5, QUAKE2, quad=MINIMAX)
+    assert_bitexact(y, R.softmax_rows_ordered(x, cols, plan, 0.5, QUAKE2, quad=MINIMAX), "minimax")
