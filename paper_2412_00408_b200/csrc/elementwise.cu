@@ -202,7 +202,7 @@ __device__ __forceinline__ float4 apply4_checked(float4 v, const EwParams& p) {
 // grid-stride loop and 6.2 for a persistent TMA bulk pipeline). The < 4
 // leading elements (`head`) and the < 4 trailing ones go scalar in CTA 0.
 template <EwOp OP, bool X86, int U>
-__global__ void __launch_bounds__(kThreads) ew_vec_kernel(const float* __restrict__ in,
+__global__ void __launch_bounds__(kThreads, 4) ew_vec_kernel(const float* __restrict__ in,
                                                           float* __restrict__ out, size_t n,
                                                           size_t head, EwParams p) {
   pdl_entry();
